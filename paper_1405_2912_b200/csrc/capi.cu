@@ -1,0 +1,111 @@
+// Library-level entry points of libhetft: initialisation, peer access,
+// error reporting.  The device model of the reference (simulated units and
+// memory spaces, src/hetrt/devices.py:54-62, :126-166, fleets.py:17-36) maps
+// onto real CUDA devices here: one memory space per device ordinal, peer
+// access enabled all-to-all over NVLink/NVSwitch when requested.
+#include "common.cuh"
+
+#include <mutex>
+#include <string.h>
+
+namespace hf {
+
+static thread_local char g_err[1024] = {0};
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+void clear_error() { g_err[0] = 0; }
+
+static std::mutex g_mu;
+static int g_sms[64] = {0};
+static int g_peer[64][64] = {{0}};
+
+int num_sms(int device) {
+    if (device < 0 || device >= 64) return kNumSMs;
+    int v = __atomic_load_n(&g_sms[device], __ATOMIC_ACQUIRE);
+    if (v > 0) return v;
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess ||
+        sms <= 0)
+        sms = kNumSMs;
+    __atomic_store_n(&g_sms[device], sms, __ATOMIC_RELEASE);
+    return sms;
+}
+
+int elem_size(int dtype) {
+    switch (dtype) {
+        case HF_F32: return 4;
+        case HF_F64: return 8;
+        case HF_U8: return 1;
+        case HF_U16: return 2;
+        case HF_U32: return 4;
+        case HF_U64: return 8;
+        default: return -1;
+    }
+}
+
+}  // namespace hf
+
+extern "C" {
+
+const char* hf_last_error(void) { return hf::g_err; }
+
+int hf_version(void) { return 1; }
+
+int hf_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int hf_init(int ndev, int enable_peer_all) {
+    std::lock_guard<std::mutex> lk(hf::g_mu);
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        hf::set_error("hf_init: no CUDA device available (%s)",
+                      e == cudaSuccess ? "count=0" : cudaGetErrorString(e));
+        return HF_ENOINIT;
+    }
+    if (ndev <= 0 || ndev > count) ndev = count;
+    if (ndev > 64) ndev = 64;
+    for (int d = 0; d < ndev; ++d) {
+        hf::num_sms(d);
+        hf::g_peer[d][d] = 1;
+    }
+    if (!enable_peer_all) return HF_OK;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    for (int d = 0; d < ndev; ++d) {
+        if (cudaSetDevice(d) != cudaSuccess) continue;
+        for (int p = 0; p < ndev; ++p) {
+            if (p == d || hf::g_peer[d][p]) continue;
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, d, p);
+            if (!can) continue;
+            cudaError_t pe = cudaDeviceEnablePeerAccess(p, 0);
+            if (pe == cudaSuccess || pe == cudaErrorPeerAccessAlreadyEnabled) {
+                hf::g_peer[d][p] = 1;
+            }
+            cudaGetLastError();  // clear "already enabled"
+        }
+    }
+    cudaSetDevice(prev);
+    return HF_OK;
+}
+
+int hf_peer_enabled(int dev, int peer) {
+    if (dev < 0 || peer < 0 || dev >= 64 || peer >= 64) return 0;
+    return hf::g_peer[dev][peer];
+}
+
+}  // extern "C"

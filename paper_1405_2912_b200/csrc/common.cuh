@@ -1,0 +1,97 @@
+// Shared helpers for libhetft (sm_100a).  Error plumbing for the C-ABI,
+// stream/device guards and small device utilities.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdarg.h>
+#include "../../include/hetft.h"
+
+namespace hf {
+
+// Thread-local last-error message (hf_last_error).
+void set_error(const char* fmt, ...);
+void clear_error();
+
+constexpr int kNumSMs = 148;  // B200: 2 dies x 74 SMs (queried at init; this is the default)
+int num_sms(int device);
+
+// RAII device guard: switches the calling thread's current device and
+// restores it on scope exit.
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (dev >= 0 && dev != prev) ok = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int elem_size(int dtype);  // bytes per element or -1
+
+}  // namespace hf
+
+#define HF_CUDA_CHECK(expr)                                                        \
+    do {                                                                           \
+        cudaError_t _e = (expr);                                                   \
+        if (_e != cudaSuccess) {                                                   \
+            hf::set_error("%s:%d: %s -> %s", __FILE__, __LINE__, #expr,            \
+                          cudaGetErrorString(_e));                                 \
+            return HF_ECUDA;                                                       \
+        }                                                                          \
+    } while (0)
+
+#define HF_CHECK_LAUNCH()                                                          \
+    do {                                                                           \
+        cudaError_t _e = cudaGetLastError();                                       \
+        if (_e != cudaSuccess) {                                                   \
+            hf::set_error("%s:%d: kernel launch failed: %s", __FILE__, __LINE__,   \
+                          cudaGetErrorString(_e));                                 \
+            return HF_ECUDA;                                                       \
+        }                                                                          \
+    } while (0)
+
+#define HF_REQUIRE(cond, ...)                                                      \
+    do {                                                                           \
+        if (!(cond)) {                                                             \
+            hf::set_error(__VA_ARGS__);                                            \
+            return HF_EINVAL;                                                      \
+        }                                                                          \
+    } while (0)
+
+// ---- device utilities ----------------------------------------------------
+namespace hf {
+
+// 128-bit streaming load that does not allocate in L1 (read-once data).
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+// 128-bit coherent load (peer / host mapped memory may be written by others;
+// also used where the non-coherent path is not allowed).
+__device__ __forceinline__ uint4 ld_plain(const uint4* p) {
+    uint4 r;
+    asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+// 128-bit streaming store (evict-first: written once, not re-read soon).
+__device__ __forceinline__ void st_stream(uint4* p, uint4 v) {
+    asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+}  // namespace hf

@@ -1,0 +1,710 @@
+// hf_vote: K-replica heterogeneity-aware majority voter (sm_100a).
+//
+// Reference semantics (paths relative to /root/reference/pkg):
+//   src/hetrt/voting.py:68-81  _compare_floats — per element, in binary64:
+//        ok  = (|a-b| <= δ·max(|a|,|b|)) & isfinite(|a-b|)
+//        ok |= a == b ;  ok |= isnan(a) & isnan(b)
+//   src/hetrt/voting.py:96-103 integer areas compare bitwise
+//   src/hetrt/voting.py:84-95  first diverging index
+// generalised to K replicas by SURVEY.md Appendix A (reduces to the
+// reference verdict / first divergence at K = 2):
+//   agree_r  = #{s != r : P(r,s,i)};  r in majority iff 2(agree_r+1) > K
+//   v(i)     = lowest majority replica; voted[i] = x_v[i] (bit copy)
+//   no majority -> unresolved, voted[i] = x_0[i], every replica counts
+//   mismatch[r] = #{i : unresolved(i) or !P(r, v(i), i)}
+//   first_div   = min{i : unresolved(i) or exists r: !P(r, v(i), i)}
+//   winner      = argmin mismatch (ties -> lowest r)
+//
+// Design (B200): one pass over all K replicas, 128-bit streaming loads
+// (ld.global.nc.L1::no_allocate; peer-device pointers are loaded directly
+// over NVLink), counts kept in registers, warp reduction with
+// __reduce_add_sync, ballot-gated first-divergence min, one atomic per block,
+// and a last-block epilogue that finalises the result and re-arms the
+// workspace so back-to-back votes need a single launch each.
+#include "common.cuh"
+
+#include <mutex>
+#include <vector>
+
+namespace hf {
+
+struct VoteWorkspace {
+    unsigned long long mismatch[HF_MAX_K];
+    unsigned long long unresolved;
+    unsigned long long first_div;  // min index; ~0ull = none
+    unsigned int ticket;
+    unsigned int pad;
+};
+
+constexpr int kMaxPairs = HF_MAX_K * (HF_MAX_K - 1) / 2;
+
+struct VoteParams {
+    const uint8_t* rep[HF_MAX_K];
+    uint8_t* voted;
+    int64_t n;      // elements
+    int64_t nvec;   // 16-byte vectors handled by the vector loop
+    double pdelta[kMaxPairs];   // max(δ_r, δ_s) per pair (r<s)
+    long long pulp[kMaxPairs];  // max(u_r, u_s) per pair, < 0 = ULP rule off
+    hf_vote_result* out;
+    VoteWorkspace* ws;
+};
+
+template <int K>
+__host__ __device__ constexpr int pair_index(int r, int s) {
+    return r * K - r * (r + 1) / 2 + (s - r - 1);
+}
+
+// ---- element predicates ---------------------------------------------------
+
+// binary64 relative rule of voting.py:74-79; inputs already widened exactly.
+__device__ __forceinline__ bool rel_ok(double a, double b, double delta) {
+    double diff = fabs(a - b);
+    double bound = delta * fmax(fabs(a), fabs(b));
+    // fmax ignores a NaN operand where numpy.maximum propagates it, but a NaN
+    // operand makes diff NaN, so (diff <= bound) and isfinite(diff) are both
+    // false either way.
+    bool ok = (diff <= bound) && isfinite(diff);
+    ok |= (a == b);
+    ok |= (isnan(a) && isnan(b));
+    return ok;
+}
+
+__device__ __forceinline__ long long ord32(uint32_t bits) {
+    int32_t i = static_cast<int32_t>(bits);
+    return i >= 0 ? static_cast<long long>(i) : (-2147483648LL - static_cast<long long>(i));
+}
+
+__device__ __forceinline__ bool ulp_ok32(uint32_t a, uint32_t b, long long u) {
+    float fa = __uint_as_float(a), fb = __uint_as_float(b);
+    if (isnan(fa) || isnan(fb)) return false;
+    long long d = ord32(a) - ord32(b);
+    if (d < 0) d = -d;
+    return d <= u;
+}
+
+__device__ __forceinline__ bool ulp_ok64(uint64_t a, uint64_t b, long long u) {
+    double fa = __longlong_as_double(static_cast<long long>(a));
+    double fb = __longlong_as_double(static_cast<long long>(b));
+    if (isnan(fa) || isnan(fb)) return false;
+    long long ia = static_cast<long long>(a), ib = static_cast<long long>(b);
+    // ordered integers; INT64_MIN - i cannot overflow for i < 0
+    long long oa = ia >= 0 ? ia : (static_cast<long long>(0x8000000000000000ull) - ia);
+    long long ob = ib >= 0 ? ib : (static_cast<long long>(0x8000000000000000ull) - ib);
+    unsigned long long d = oa >= ob ? static_cast<unsigned long long>(oa) - static_cast<unsigned long long>(ob)
+                                    : static_cast<unsigned long long>(ob) - static_cast<unsigned long long>(oa);
+    return d <= static_cast<unsigned long long>(u);
+}
+
+// Element traits: raw bit container and pair predicate.
+template <int DT>
+struct Elem;
+
+template <>
+struct Elem<HF_F32> {
+    using T = uint32_t;
+    static constexpr int kPerVec = 4;
+    __device__ static __forceinline__ bool ok(T a, T b, double delta, long long ulp) {
+        if (a == b) return true;  // bit-identical (incl. identical NaN payloads)
+        bool r = rel_ok(static_cast<double>(__uint_as_float(a)),
+                        static_cast<double>(__uint_as_float(b)), delta);
+        if (!r && ulp >= 0) r = ulp_ok32(a, b, ulp);
+        return r;
+    }
+};
+
+template <>
+struct Elem<HF_F64> {
+    using T = uint64_t;
+    static constexpr int kPerVec = 2;
+    __device__ static __forceinline__ bool ok(T a, T b, double delta, long long ulp) {
+        if (a == b) return true;
+        bool r = rel_ok(__longlong_as_double(static_cast<long long>(a)),
+                        __longlong_as_double(static_cast<long long>(b)), delta);
+        if (!r && ulp >= 0) r = ulp_ok64(a, b, ulp);
+        return r;
+    }
+};
+
+template <typename U, int PV>
+struct IntElem {
+    using T = U;
+    static constexpr int kPerVec = PV;
+    __device__ static __forceinline__ bool ok(T a, T b, double, long long) { return a == b; }
+};
+template <> struct Elem<HF_U8> : IntElem<uint8_t, 16> {};
+template <> struct Elem<HF_U16> : IntElem<uint16_t, 8> {};
+template <> struct Elem<HF_U32> : IntElem<uint32_t, 4> {};
+template <> struct Elem<HF_U64> : IntElem<uint64_t, 2> {};
+
+template <typename T, int PV>
+__device__ __forceinline__ T extract(const uint4& v, int e) {
+    if constexpr (sizeof(T) == 4) {
+        return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
+    } else if constexpr (sizeof(T) == 8) {
+        return e == 0 ? (static_cast<uint64_t>(v.y) << 32 | v.x)
+                      : (static_cast<uint64_t>(v.w) << 32 | v.z);
+    } else if constexpr (sizeof(T) == 2) {
+        uint32_t w = (e >> 1) == 0 ? v.x : (e >> 1) == 1 ? v.y : (e >> 1) == 2 ? v.z : v.w;
+        return static_cast<T>(w >> (16 * (e & 1)));
+    } else {
+        uint32_t w = (e >> 2) == 0 ? v.x : (e >> 2) == 1 ? v.y : (e >> 2) == 2 ? v.z : v.w;
+        return static_cast<T>(w >> (8 * (e & 3)));
+    }
+}
+
+// Per-thread accumulators.
+template <int K>
+struct Acc {
+    uint32_t mism[K];
+    uint32_t unres;
+    unsigned long long first;
+};
+
+// Vote one element given its K raw values; returns the voted raw value.
+template <int DT, int K>
+__device__ __forceinline__ typename Elem<DT>::T vote_elem(const typename Elem<DT>::T (&x)[K],
+                                                           const VoteParams& p, Acc<K>& acc,
+                                                           unsigned long long idx) {
+    using E = Elem<DT>;
+    uint32_t agree[K];
+#pragma unroll
+    for (int r = 0; r < K; ++r) agree[r] = 1u << r;
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+#pragma unroll
+        for (int s = r + 1; s < K; ++s) {
+            const int pi = pair_index<K>(r, s);
+            if (E::ok(x[r], x[s], p.pdelta[pi], p.pulp[pi])) {
+                agree[r] |= 1u << s;
+                agree[s] |= 1u << r;
+            }
+        }
+    }
+    int v = -1;
+#pragma unroll
+    for (int r = K - 1; r >= 0; --r) {
+        // 2*(agree_r + 1) > K with agree_r counted without self
+        if (2 * __popc(agree[r]) > K) v = r;
+    }
+    typename E::T out = x[0];
+    bool flag;
+    if (v < 0) {
+#pragma unroll
+        for (int r = 0; r < K; ++r) acc.mism[r] += 1;
+        acc.unres += 1;
+        flag = true;
+    } else {
+        uint32_t m = 0;
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+            if (v == r) {
+                m = agree[r];
+                out = x[r];
+            }
+        }
+        const uint32_t full = (1u << K) - 1u;
+#pragma unroll
+        for (int r = 0; r < K; ++r) acc.mism[r] += ((m >> r) & 1u) ^ 1u;
+        flag = (m & full) != full;
+    }
+    if (flag && acc.first == ~0ull) acc.first = idx;
+    return out;
+}
+
+template <int DT, int K, int UNROLL>
+__global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteParams p) {
+    using E = Elem<DT>;
+    using T = typename E::T;
+    constexpr int PV = E::kPerVec;
+
+    Acc<K> acc;
+#pragma unroll
+    for (int r = 0; r < K; ++r) acc.mism[r] = 0;
+    acc.unres = 0;
+    acc.first = ~0ull;
+
+    const long long gtid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long long gstride = static_cast<long long>(gridDim.x) * blockDim.x;
+
+    // ---- vector loop: UNROLL x K 128-bit loads in flight per thread ----
+    long long j = gtid;
+    for (; j + (UNROLL - 1) * gstride < p.nvec; j += UNROLL * gstride) {
+        uint4 v[UNROLL][K];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u)
+#pragma unroll
+            for (int r = 0; r < K; ++r)
+                v[u][r] = ld_stream(reinterpret_cast<const uint4*>(p.rep[r]) + (j + u * gstride));
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+            const long long vj = j + u * gstride;
+            T o[PV];
+#pragma unroll
+            for (int e = 0; e < PV; ++e) {
+                T x[K];
+#pragma unroll
+                for (int r = 0; r < K; ++r) x[r] = extract<T, PV>(v[u][r], e);
+                o[e] = vote_elem<DT, K>(x, p, acc, static_cast<unsigned long long>(vj) * PV + e);
+            }
+            if (p.voted != nullptr) {
+                uint4 w;
+                if constexpr (sizeof(T) == 4) {
+                    w = make_uint4(o[0], o[1], o[2], o[3]);
+                } else if constexpr (sizeof(T) == 8) {
+                    w = make_uint4(static_cast<uint32_t>(o[0]), static_cast<uint32_t>(o[0] >> 32),
+                                   static_cast<uint32_t>(o[1]), static_cast<uint32_t>(o[1] >> 32));
+                } else if constexpr (sizeof(T) == 2) {
+                    uint32_t ww[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        ww[q] = static_cast<uint32_t>(o[2 * q]) | (static_cast<uint32_t>(o[2 * q + 1]) << 16);
+                    w = make_uint4(ww[0], ww[1], ww[2], ww[3]);
+                } else {
+                    uint32_t ww[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        ww[q] = static_cast<uint32_t>(o[4 * q]) | (static_cast<uint32_t>(o[4 * q + 1]) << 8) |
+                                (static_cast<uint32_t>(o[4 * q + 2]) << 16) |
+                                (static_cast<uint32_t>(o[4 * q + 3]) << 24);
+                    w = make_uint4(ww[0], ww[1], ww[2], ww[3]);
+                }
+                st_stream(reinterpret_cast<uint4*>(p.voted) + vj, w);
+            }
+        }
+    }
+    // remainder vectors (fewer than UNROLL strides left)
+    for (; j < p.nvec; j += gstride) {
+        uint4 v[K];
+#pragma unroll
+        for (int r = 0; r < K; ++r) v[r] = ld_stream(reinterpret_cast<const uint4*>(p.rep[r]) + j);
+        T o[PV];
+#pragma unroll
+        for (int e = 0; e < PV; ++e) {
+            T x[K];
+#pragma unroll
+            for (int r = 0; r < K; ++r) x[r] = extract<T, PV>(v[r], e);
+            o[e] = vote_elem<DT, K>(x, p, acc, static_cast<unsigned long long>(j) * PV + e);
+        }
+        if (p.voted != nullptr) {
+            T* dst = reinterpret_cast<T*>(p.voted) + j * PV;
+#pragma unroll
+            for (int e = 0; e < PV; ++e) dst[e] = o[e];
+        }
+    }
+    // ---- scalar tail (and the whole buffer when pointers are unaligned) ----
+    for (long long i = p.nvec * PV + gtid; i < p.n; i += gstride) {
+        T x[K];
+#pragma unroll
+        for (int r = 0; r < K; ++r) x[r] = __ldg(reinterpret_cast<const T*>(p.rep[r]) + i);
+        T o = vote_elem<DT, K>(x, p, acc, static_cast<unsigned long long>(i));
+        if (p.voted != nullptr) reinterpret_cast<T*>(p.voted)[i] = o;
+    }
+
+    // ---- reduction: warp -> block (smem) -> one atomic per block ----------
+    __shared__ unsigned long long s_cnt[K + 1];
+    __shared__ unsigned long long s_first;
+    __shared__ bool s_last;
+    if (threadIdx.x <= K) s_cnt[threadIdx.x] = 0;
+    if (threadIdx.x == 0) s_first = ~0ull;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+        uint32_t t = __reduce_add_sync(0xffffffffu, acc.mism[r]);
+        if (lane == 0 && t) atomicAdd(&s_cnt[r], static_cast<unsigned long long>(t));
+    }
+    {
+        uint32_t t = __reduce_add_sync(0xffffffffu, acc.unres);
+        if (lane == 0 && t) atomicAdd(&s_cnt[K], static_cast<unsigned long long>(t));
+    }
+    if (__ballot_sync(0xffffffffu, acc.first != ~0ull)) {
+        unsigned long long f = acc.first;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            unsigned long long g = __shfl_xor_sync(0xffffffffu, f, o);
+            f = g < f ? g : f;
+        }
+        if (lane == 0) atomicMin(&s_first, f);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        VoteWorkspace* ws = p.ws;
+#pragma unroll
+        for (int r = 0; r <= K; ++r) {
+            unsigned long long c = s_cnt[r];
+            if (c) atomicAdd(r < K ? &ws->mismatch[r] : &ws->unresolved, c);
+        }
+        if (s_first != ~0ull) atomicMin(&ws->first_div, s_first);
+        __threadfence();
+        unsigned int t = atomicAdd(&ws->ticket, 1u);
+        s_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    // ---- last block: finalise the result and re-arm the workspace ----------
+    if (s_last && threadIdx.x == 0) {
+        __threadfence();
+        VoteWorkspace* ws = p.ws;
+        hf_vote_result* out = p.out;
+        volatile unsigned long long* vm = ws->mismatch;
+        long long best = -1;
+        int winner = 0;
+        bool any = false;
+        for (int r = 0; r < HF_MAX_K; ++r) {
+            long long m = r < K ? static_cast<long long>(vm[r]) : 0;
+            out->mismatch[r] = m;
+            if (r < K) {
+                if (best < 0 || m < best) {
+                    best = m;
+                    winner = r;
+                }
+                any |= m > 0;
+            }
+        }
+        long long unres = static_cast<long long>(*(volatile unsigned long long*)&ws->unresolved);
+        unsigned long long fd = *(volatile unsigned long long*)&ws->first_div;
+        out->unresolved = unres;
+        out->first_div = fd == ~0ull ? -1 : static_cast<long long>(fd);
+        out->winner = winner;
+        out->verdict = unres > 0 ? HF_VERDICT_MISMATCH : (any ? HF_VERDICT_CORRECTED : HF_VERDICT_MATCH);
+        out->K = K;
+        out->reserved = 0;
+        for (int r = 0; r < HF_MAX_K; ++r) ws->mismatch[r] = 0;
+        ws->unresolved = 0;
+        ws->first_div = ~0ull;
+        __threadfence();
+        ws->ticket = 0;
+    }
+}
+
+// Arbitrary-width integer areas (ValueType.INT with width not in {1,2,4,8}):
+// element-granular, byte loop.  Same majority contract with P = bytewise eq.
+template <int K>
+__global__ void __launch_bounds__(256) vote_bytes_kernel(const __grid_constant__ VoteParams p, int width) {
+    Acc<K> acc;
+#pragma unroll
+    for (int r = 0; r < K; ++r) acc.mism[r] = 0;
+    acc.unres = 0;
+    acc.first = ~0ull;
+    const long long gtid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long long gstride = static_cast<long long>(gridDim.x) * blockDim.x;
+    for (long long i = gtid; i < p.n; i += gstride) {
+        uint32_t agree[K];
+#pragma unroll
+        for (int r = 0; r < K; ++r) agree[r] = 1u << r;
+#pragma unroll
+        for (int r = 0; r < K; ++r)
+#pragma unroll
+            for (int s = r + 1; s < K; ++s) {
+                bool eq = true;
+                for (int b = 0; b < width && eq; ++b)
+                    eq = p.rep[r][i * width + b] == p.rep[s][i * width + b];
+                if (eq) {
+                    agree[r] |= 1u << s;
+                    agree[s] |= 1u << r;
+                }
+            }
+        int v = -1;
+#pragma unroll
+        for (int r = K - 1; r >= 0; --r)
+            if (2 * __popc(agree[r]) > K) v = r;
+        bool flag;
+        int src = 0;
+        if (v < 0) {
+#pragma unroll
+            for (int r = 0; r < K; ++r) acc.mism[r] += 1;
+            acc.unres += 1;
+            flag = true;
+        } else {
+            uint32_t m = agree[v];
+            src = v;
+            const uint32_t full = (1u << K) - 1u;
+#pragma unroll
+            for (int r = 0; r < K; ++r) acc.mism[r] += ((m >> r) & 1u) ^ 1u;
+            flag = (m & full) != full;
+        }
+        if (flag && acc.first == ~0ull) acc.first = i;
+        if (p.voted != nullptr)
+            for (int b = 0; b < width; ++b) p.voted[i * width + b] = p.rep[src][i * width + b];
+    }
+    __shared__ unsigned long long s_cnt[K + 1];
+    __shared__ unsigned long long s_first;
+    __shared__ bool s_last;
+    if (threadIdx.x <= K) s_cnt[threadIdx.x] = 0;
+    if (threadIdx.x == 0) s_first = ~0ull;
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < K; ++r)
+        if (acc.mism[r]) atomicAdd(&s_cnt[r], static_cast<unsigned long long>(acc.mism[r]));
+    if (acc.unres) atomicAdd(&s_cnt[K], static_cast<unsigned long long>(acc.unres));
+    if (acc.first != ~0ull) atomicMin(&s_first, acc.first);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        VoteWorkspace* ws = p.ws;
+        for (int r = 0; r <= K; ++r)
+            if (s_cnt[r]) atomicAdd(r < K ? &ws->mismatch[r] : &ws->unresolved, s_cnt[r]);
+        if (s_first != ~0ull) atomicMin(&ws->first_div, s_first);
+        __threadfence();
+        unsigned int t = atomicAdd(&ws->ticket, 1u);
+        s_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+        __threadfence();
+        VoteWorkspace* ws = p.ws;
+        hf_vote_result* out = p.out;
+        volatile unsigned long long* vm = ws->mismatch;
+        long long best = -1;
+        int winner = 0;
+        bool any = false;
+        for (int r = 0; r < HF_MAX_K; ++r) {
+            long long m = r < K ? static_cast<long long>(vm[r]) : 0;
+            out->mismatch[r] = m;
+            if (r < K) {
+                if (best < 0 || m < best) {
+                    best = m;
+                    winner = r;
+                }
+                any |= m > 0;
+            }
+        }
+        long long unres = static_cast<long long>(*(volatile unsigned long long*)&ws->unresolved);
+        unsigned long long fd = *(volatile unsigned long long*)&ws->first_div;
+        out->unresolved = unres;
+        out->first_div = fd == ~0ull ? -1 : static_cast<long long>(fd);
+        out->winner = winner;
+        out->verdict = unres > 0 ? HF_VERDICT_MISMATCH : (any ? HF_VERDICT_CORRECTED : HF_VERDICT_MATCH);
+        out->K = K;
+        out->reserved = 0;
+        for (int r = 0; r < HF_MAX_K; ++r) ws->mismatch[r] = 0;
+        ws->unresolved = 0;
+        ws->first_div = ~0ull;
+        __threadfence();
+        ws->ticket = 0;
+    }
+}
+
+__global__ void ws_init_kernel(VoteWorkspace* ws) {
+    for (int r = 0; r < HF_MAX_K; ++r) ws->mismatch[r] = 0;
+    ws->unresolved = 0;
+    ws->first_div = ~0ull;
+    ws->ticket = 0;
+    ws->pad = 0;
+}
+
+// ---- launch ----------------------------------------------------------------
+
+using VoteKernel = void (*)(VoteParams);
+
+template <int DT>
+static VoteKernel pick_kernel(int K) {
+    switch (K) {
+        case 2: return vote_kernel<DT, 2, 2>;
+        case 3: return vote_kernel<DT, 3, 2>;
+        case 4: return vote_kernel<DT, 4, 2>;
+        case 5: return vote_kernel<DT, 5, 2>;
+        case 6: return vote_kernel<DT, 6, 1>;
+        case 7: return vote_kernel<DT, 7, 1>;
+        case 8: return vote_kernel<DT, 8, 1>;
+        default: return nullptr;
+    }
+}
+
+static VoteKernel select_kernel(int dtype, int K) {
+    switch (dtype) {
+        case HF_F32: return pick_kernel<HF_F32>(K);
+        case HF_F64: return pick_kernel<HF_F64>(K);
+        case HF_U8: return pick_kernel<HF_U8>(K);
+        case HF_U16: return pick_kernel<HF_U16>(K);
+        case HF_U32: return pick_kernel<HF_U32>(K);
+        case HF_U64: return pick_kernel<HF_U64>(K);
+        default: return nullptr;
+    }
+}
+
+static int fill_params(VoteParams& p, const void* const* replicas, int K, int64_t n, int width,
+                       const double* rel_tol, const int32_t* ulp_tol, void* voted) {
+    HF_REQUIRE(replicas != nullptr, "hf_vote: replicas is NULL");
+    HF_REQUIRE(K >= 2 && K <= HF_MAX_K, "hf_vote: K=%d outside [2, %d]", K, HF_MAX_K);
+    HF_REQUIRE(n >= 0, "hf_vote: negative n");
+    memset(&p, 0, sizeof(p));
+    bool aligned = (voted == nullptr) || (reinterpret_cast<uintptr_t>(voted) % 16 == 0);
+    for (int r = 0; r < K; ++r) {
+        HF_REQUIRE(replicas[r] != nullptr || n == 0, "hf_vote: replica %d is NULL", r);
+        HF_REQUIRE(reinterpret_cast<uintptr_t>(replicas[r]) % (width > 8 ? 1 : width) == 0,
+                   "hf_vote: replica %d not aligned to its element size", r);
+        p.rep[r] = static_cast<const uint8_t*>(replicas[r]);
+        aligned &= reinterpret_cast<uintptr_t>(replicas[r]) % 16 == 0;
+    }
+    p.voted = static_cast<uint8_t*>(voted);
+    p.n = n;
+    const int per_vec = width <= 8 ? 16 / width : 0;
+    p.nvec = (aligned && per_vec > 0) ? n / per_vec : 0;
+    for (int r = 0; r < K; ++r)
+        for (int s = r + 1; s < K; ++s) {
+            int pi = r * K - r * (r + 1) / 2 + (s - r - 1);
+            double dr = rel_tol ? rel_tol[r] : 0.0, ds = rel_tol ? rel_tol[s] : 0.0;
+            HF_REQUIRE(!(dr < 0) && !(ds < 0), "hf_vote: negative relative tolerance");
+            p.pdelta[pi] = dr > ds ? dr : ds;
+            if (ulp_tol) {
+                long long ur = ulp_tol[r], us = ulp_tol[s];
+                p.pulp[pi] = ur > us ? ur : us;
+            } else {
+                p.pulp[pi] = -1;
+            }
+        }
+    return HF_OK;
+}
+
+static int launch_vote(VoteParams& p, int K, int dtype, int width, int device, cudaStream_t st) {
+    int sms = num_sms(device);
+    const int threads = 256;
+    long long work = p.nvec > 0 ? p.nvec : p.n;
+    long long want = (work + threads - 1) / threads;
+    if (want < 1) want = 1;
+    long long cap = static_cast<long long>(sms) * 8;
+    int grid = static_cast<int>(want < cap ? want : cap);
+    if (dtype >= 0) {
+        VoteKernel k = select_kernel(dtype, K);
+        HF_REQUIRE(k != nullptr, "hf_vote: unsupported dtype %d / K %d", dtype, K);
+        k<<<grid, threads, 0, st>>>(p);
+    } else {
+        switch (K) {
+            case 2: vote_bytes_kernel<2><<<grid, threads, 0, st>>>(p, width); break;
+            case 3: vote_bytes_kernel<3><<<grid, threads, 0, st>>>(p, width); break;
+            case 4: vote_bytes_kernel<4><<<grid, threads, 0, st>>>(p, width); break;
+            case 5: vote_bytes_kernel<5><<<grid, threads, 0, st>>>(p, width); break;
+            case 6: vote_bytes_kernel<6><<<grid, threads, 0, st>>>(p, width); break;
+            case 7: vote_bytes_kernel<7><<<grid, threads, 0, st>>>(p, width); break;
+            case 8: vote_bytes_kernel<8><<<grid, threads, 0, st>>>(p, width); break;
+        }
+    }
+    HF_CHECK_LAUNCH();
+    return HF_OK;
+}
+
+// Per-device pool of (workspace, device result) slots for the synchronous API.
+struct SyncSlot {
+    VoteWorkspace* ws = nullptr;
+    hf_vote_result* dres = nullptr;
+    hf_vote_result* hres = nullptr;  // pinned
+};
+static std::mutex g_pool_mu;
+static std::vector<SyncSlot> g_pool[64];
+
+static int acquire_slot(int device, SyncSlot& out) {
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        if (!g_pool[device].empty()) {
+            out = g_pool[device].back();
+            g_pool[device].pop_back();
+            return HF_OK;
+        }
+    }
+    SyncSlot s;
+    HF_CUDA_CHECK(cudaMalloc(&s.ws, sizeof(VoteWorkspace)));
+    HF_CUDA_CHECK(cudaMalloc(&s.dres, sizeof(hf_vote_result)));
+    HF_CUDA_CHECK(cudaMallocHost(&s.hres, sizeof(hf_vote_result)));
+    ws_init_kernel<<<1, 1>>>(s.ws);
+    HF_CHECK_LAUNCH();
+    HF_CUDA_CHECK(cudaDeviceSynchronize());
+    out = s;
+    return HF_OK;
+}
+
+static void release_slot(int device, const SyncSlot& s) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    g_pool[device].push_back(s);
+}
+
+static int vote_sync(const void* const* replicas, int K, int64_t n, int dtype, int width,
+                     const double* rel_tol, const int32_t* ulp_tol, void* voted,
+                     hf_vote_result* out, int device, void* stream) {
+    HF_REQUIRE(out != nullptr, "hf_vote: out is NULL");
+    HF_REQUIRE(device >= 0 && device < 64, "hf_vote: bad device %d", device);
+    VoteParams p;
+    int rc = fill_params(p, replicas, K, n, width, rel_tol, ulp_tol, voted);
+    if (rc) return rc;
+    if (n == 0) {
+        memset(out, 0, sizeof(*out));
+        out->first_div = -1;
+        out->K = K;
+        out->verdict = HF_VERDICT_MATCH;
+        return HF_OK;
+    }
+    DeviceGuard g(device);
+    HF_REQUIRE(g.ok, "hf_vote: cannot select device %d", device);
+    SyncSlot slot;
+    rc = acquire_slot(device, slot);
+    if (rc) return rc;
+    cudaStream_t st = as_stream(stream);
+    p.ws = slot.ws;
+    p.out = slot.dres;
+    rc = launch_vote(p, K, dtype, width, device, st);
+    if (rc == HF_OK) {
+        cudaError_t e = cudaMemcpyAsync(slot.hres, slot.dres, sizeof(hf_vote_result),
+                                        cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) {
+            set_error("hf_vote: %s", cudaGetErrorString(e));
+            rc = HF_ECUDA;
+        } else {
+            *out = *slot.hres;
+        }
+    }
+    if (rc == HF_OK) release_slot(device, slot);  // a faulted slot is dropped, not reused
+    return rc;
+}
+
+}  // namespace hf
+
+extern "C" {
+
+int hf_vote(const void* const* replicas, int K, int64_t n, int dtype, const double* rel_tol,
+            const int32_t* ulp_tol, void* voted, hf_vote_result* out, int device, void* stream) {
+    HF_REQUIRE(hf::elem_size(dtype) > 0, "hf_vote: unknown dtype %d", dtype);
+    return hf::vote_sync(replicas, K, n, dtype, hf::elem_size(dtype), rel_tol, ulp_tol, voted, out,
+                         device, stream);
+}
+
+int hf_vote_bytes(const void* const* replicas, int K, int64_t n, int elem_width, void* voted,
+                  hf_vote_result* out, int device, void* stream) {
+    HF_REQUIRE(elem_width >= 1, "hf_vote_bytes: element width must be >= 1");
+    switch (elem_width) {
+        case 1: return hf_vote(replicas, K, n, HF_U8, nullptr, nullptr, voted, out, device, stream);
+        case 2: return hf_vote(replicas, K, n, HF_U16, nullptr, nullptr, voted, out, device, stream);
+        case 4: return hf_vote(replicas, K, n, HF_U32, nullptr, nullptr, voted, out, device, stream);
+        case 8: return hf_vote(replicas, K, n, HF_U64, nullptr, nullptr, voted, out, device, stream);
+        default:
+            return hf::vote_sync(replicas, K, n, -1, elem_width, nullptr, nullptr, voted, out,
+                                 device, stream);
+    }
+}
+
+int64_t hf_vote_workspace_bytes(void) { return static_cast<int64_t>(sizeof(hf::VoteWorkspace)); }
+
+int hf_vote_workspace_init(void* workspace, int device, void* stream) {
+    HF_REQUIRE(workspace != nullptr, "hf_vote_workspace_init: NULL workspace");
+    hf::DeviceGuard g(device);
+    HF_REQUIRE(g.ok, "hf_vote_workspace_init: cannot select device %d", device);
+    hf::ws_init_kernel<<<1, 1, 0, hf::as_stream(stream)>>>(static_cast<hf::VoteWorkspace*>(workspace));
+    HF_CHECK_LAUNCH();
+    return HF_OK;
+}
+
+int hf_vote_async(const void* const* replicas, int K, int64_t n, int dtype, const double* rel_tol,
+                  const int32_t* ulp_tol, void* voted, hf_vote_result* dev_out, void* workspace,
+                  int device, void* stream) {
+    HF_REQUIRE(hf::elem_size(dtype) > 0, "hf_vote_async: unknown dtype %d", dtype);
+    HF_REQUIRE(dev_out != nullptr && workspace != nullptr, "hf_vote_async: NULL result/workspace");
+    HF_REQUIRE(n > 0, "hf_vote_async: n must be > 0");
+    hf::VoteParams p;
+    int rc = hf::fill_params(p, replicas, K, n, hf::elem_size(dtype), rel_tol, ulp_tol, voted);
+    if (rc) return rc;
+    hf::DeviceGuard g(device);
+    HF_REQUIRE(g.ok, "hf_vote_async: cannot select device %d", device);
+    p.ws = static_cast<hf::VoteWorkspace*>(workspace);
+    p.out = dev_out;
+    return hf::launch_vote(p, K, dtype, hf::elem_size(dtype), device, hf::as_stream(stream));
+}
+
+}  // extern "C"

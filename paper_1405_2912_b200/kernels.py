@@ -1,0 +1,293 @@
+"""Torch-tensor front end of the libhetft kernels.
+
+PyTorch is plumbing here: it allocates device memory and supplies streams.
+Every function passes ``data_ptr()`` values through the C-ABI
+(include/hetft.h) and the computation runs in the sm_100a kernels of
+``csrc/``.  Nothing here computes on the CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import torch
+
+from . import _lib
+from ._lib import HfVoteResult, check
+
+_TORCH_DTYPE = {
+    torch.float32: _lib.HF_F32,
+    torch.float64: _lib.HF_F64,
+    torch.uint8: _lib.HF_U8,
+    torch.int8: _lib.HF_U8,
+    torch.int16: _lib.HF_U16,
+    torch.uint16: _lib.HF_U16,
+    torch.int32: _lib.HF_U32,
+    torch.uint32: _lib.HF_U32,
+    torch.int64: _lib.HF_U64,
+    torch.uint64: _lib.HF_U64,
+}
+
+
+def hf_dtype(t: torch.Tensor) -> int:
+    try:
+        return _TORCH_DTYPE[t.dtype]
+    except KeyError:
+        raise ValueError(f"unsupported element type {t.dtype}") from None
+
+
+def _stream_ptr(device: int, stream: Optional[torch.cuda.Stream]) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    return int(s.cuda_stream)
+
+
+def _dev(t: torch.Tensor) -> int:
+    if t.device.type != "cuda":
+        raise ValueError(f"tensor on {t.device}; libhetft kernels need CUDA tensors")
+    return t.device.index if t.device.index is not None else torch.cuda.current_device()
+
+
+@dataclass
+class VoteResult:
+    """Outcome of one K-replica vote."""
+
+    verdict: str                      # "match" | "corrected" | "mismatch"
+    mismatch: list[int]
+    unresolved: int
+    first_div: int                    # -1 when every replica agrees everywhere
+    winner: int
+    K: int
+    faulty: list[int] = field(default_factory=list)
+
+    @classmethod
+    def from_c(cls, r: HfVoteResult) -> "VoteResult":
+        K = int(r.K)
+        mism = [int(r.mismatch[i]) for i in range(K)]
+        return cls(_lib.VERDICT_NAMES[int(r.verdict)], mism, int(r.unresolved), int(r.first_div),
+                   int(r.winner), K, [i for i, m in enumerate(mism) if m > 0])
+
+
+def _ptr_array(ts: Sequence[torch.Tensor]):
+    arr = (ctypes.c_void_p * len(ts))()
+    for i, t in enumerate(ts):
+        arr[i] = t.data_ptr()
+    return arr
+
+
+def _tolerances(K: int, rel_tol, ulp_tol):
+    if isinstance(rel_tol, (int, float)):
+        rel = [float(rel_tol)] * K
+    else:
+        rel = [float(x) for x in rel_tol]
+    if len(rel) != K:
+        raise ValueError(f"rel_tol has {len(rel)} entries for {K} replicas")
+    rel_c = (ctypes.c_double * K)(*rel)
+    if ulp_tol is None:
+        return rel_c, None
+    ulp = [int(ulp_tol)] * K if isinstance(ulp_tol, int) else [int(x) for x in ulp_tol]
+    if len(ulp) != K:
+        raise ValueError(f"ulp_tol has {len(ulp)} entries for {K} replicas")
+    return rel_c, (ctypes.c_int32 * K)(*ulp)
+
+
+def vote(replicas: Sequence[torch.Tensor], rel_tol=0.001, ulp_tol=None,
+         voted: Optional[torch.Tensor] = None, device: Optional[int] = None,
+         stream: Optional[torch.cuda.Stream] = None) -> VoteResult:
+    """K-replica vote.  Replicas may live on different GPUs: the kernel runs
+    on `device` (default: voted's or replica 0's) and loads peer buffers
+    directly over NVLink when peer access is enabled."""
+    K = len(replicas)
+    if not 2 <= K <= _lib.HF_MAX_K:
+        raise ValueError(f"need 2..{_lib.HF_MAX_K} replicas, got {K}")
+    n = replicas[0].numel()
+    dt = replicas[0].dtype
+    for r in replicas:
+        if r.numel() != n or r.dtype != dt:
+            raise ValueError("replicas differ in size or element type")
+        if not r.is_contiguous():
+            raise ValueError("replicas must be contiguous")
+    if voted is not None and (voted.numel() != n or voted.dtype != dt or not voted.is_contiguous()):
+        raise ValueError("voted buffer must match the replicas")
+    if device is None:
+        device = _dev(voted) if voted is not None else _dev(replicas[0])
+    _lib.init()
+    rel_c, ulp_c = _tolerances(K, rel_tol, ulp_tol)
+    out = HfVoteResult()
+    lib = _lib.load()
+    rc = lib.hf_vote(_ptr_array(replicas), K, n, hf_dtype(replicas[0]), rel_c, ulp_c,
+                     voted.data_ptr() if voted is not None else None, ctypes.byref(out),
+                     device, _stream_ptr(device, stream))
+    check("hf_vote", rc)
+    return VoteResult.from_c(out)
+
+
+def vote_bytes(replicas: Sequence[torch.Tensor], elem_width: int,
+               voted: Optional[torch.Tensor] = None, device: Optional[int] = None,
+               stream: Optional[torch.cuda.Stream] = None) -> VoteResult:
+    """Vote byte buffers holding integer elements of any width (bitwise)."""
+    K = len(replicas)
+    nbytes = replicas[0].numel() * replicas[0].element_size()
+    if nbytes % elem_width:
+        raise ValueError(f"{nbytes} bytes is not a multiple of element width {elem_width}")
+    if device is None:
+        device = _dev(voted) if voted is not None else _dev(replicas[0])
+    _lib.init()
+    out = HfVoteResult()
+    rc = _lib.load().hf_vote_bytes(_ptr_array(replicas), K, nbytes // elem_width, elem_width,
+                                   voted.data_ptr() if voted is not None else None,
+                                   ctypes.byref(out), device, _stream_ptr(device, stream))
+    check("hf_vote_bytes", rc)
+    return VoteResult.from_c(out)
+
+
+class VoteWorkspace:
+    """Device workspace + device result for hf_vote_async (no host sync)."""
+
+    def __init__(self, device: int, stream: Optional[torch.cuda.Stream] = None):
+        _lib.init()
+        lib = _lib.load()
+        self.device = device
+        nb = int(lib.hf_vote_workspace_bytes())
+        self.ws = torch.empty(nb, dtype=torch.uint8, device=f"cuda:{device}")
+        self.result = torch.zeros(ctypes.sizeof(HfVoteResult), dtype=torch.uint8,
+                                  device=f"cuda:{device}")
+        check("hf_vote_workspace_init",
+              lib.hf_vote_workspace_init(self.ws.data_ptr(), device, _stream_ptr(device, stream)))
+
+    def read(self) -> VoteResult:
+        host = self.result.cpu().numpy().tobytes()
+        return VoteResult.from_c(HfVoteResult.from_buffer_copy(host))
+
+
+def vote_async(replicas: Sequence[torch.Tensor], ws: VoteWorkspace, rel_tol=0.001, ulp_tol=None,
+               voted: Optional[torch.Tensor] = None,
+               stream: Optional[torch.cuda.Stream] = None) -> None:
+    K = len(replicas)
+    n = replicas[0].numel()
+    rel_c, ulp_c = _tolerances(K, rel_tol, ulp_tol)
+    rc = _lib.load().hf_vote_async(_ptr_array(replicas), K, n, hf_dtype(replicas[0]), rel_c, ulp_c,
+                                   voted.data_ptr() if voted is not None else None,
+                                   ws.result.data_ptr(), ws.ws.data_ptr(), ws.device,
+                                   _stream_ptr(ws.device, stream))
+    check("hf_vote_async", rc)
+
+
+# ---- copy / checkpoint ------------------------------------------------------
+
+def _nbytes(t: torch.Tensor) -> int:
+    return t.numel() * t.element_size()
+
+
+def _loc(t: torch.Tensor) -> int:
+    return _dev(t) if t.device.type == "cuda" else -1
+
+
+def copy(dst: torch.Tensor, src: torch.Tensor, stream: Optional[torch.cuda.Stream] = None) -> None:
+    """dst <- src (bytes).  Device/peer/host placement is resolved natively."""
+    nb = _nbytes(src)
+    if _nbytes(dst) != nb:
+        raise ValueError("copy: size mismatch")
+    _lib.init()
+    dd, sd = _loc(dst), _loc(src)
+    sdev = dd if dd >= 0 else sd
+    check("hf_copy", _lib.load().hf_copy(dst.data_ptr(), dd, src.data_ptr(), sd, nb,
+                                         _stream_ptr(sdev, stream) if sdev >= 0 else None))
+
+
+def checkpoint(ckpt: torch.Tensor, buf: torch.Tensor, with_checksum: bool = False,
+               stream: Optional[torch.cuda.Stream] = None) -> Optional[int]:
+    nb = _nbytes(buf)
+    if _nbytes(ckpt) != nb:
+        raise ValueError("checkpoint: size mismatch")
+    _lib.init()
+    dev = _dev(buf)
+    cs = ctypes.c_uint64(0)
+    check("hf_checkpoint", _lib.load().hf_checkpoint(
+        ckpt.data_ptr(), buf.data_ptr(), nb, ctypes.byref(cs) if with_checksum else None, dev,
+        _stream_ptr(dev, stream)))
+    return int(cs.value) if with_checksum else None
+
+
+def restore(buf: torch.Tensor, ckpt: torch.Tensor, expect: Optional[int] = None,
+            stream: Optional[torch.cuda.Stream] = None) -> None:
+    nb = _nbytes(buf)
+    if _nbytes(ckpt) != nb:
+        raise ValueError("restore: size mismatch")
+    _lib.init()
+    dev = _dev(buf)
+    ex = ctypes.c_uint64(expect) if expect is not None else None
+    check("hf_restore", _lib.load().hf_restore(buf.data_ptr(), ckpt.data_ptr(), nb,
+                                               ctypes.byref(ex) if ex is not None else None, dev,
+                                               _stream_ptr(dev, stream)))
+
+
+def checksum(buf: torch.Tensor, stream: Optional[torch.cuda.Stream] = None) -> int:
+    _lib.init()
+    dev = _dev(buf)
+    out = ctypes.c_uint64(0)
+    check("hf_checksum", _lib.load().hf_checksum(buf.data_ptr(), _nbytes(buf), ctypes.byref(out),
+                                                 dev, _stream_ptr(dev, stream)))
+    return int(out.value)
+
+
+# ---- fault injection ----------------------------------------------------------
+
+def inject_bitflip(buf: torch.Tensor, elem: int, bit: int,
+                   stream: Optional[torch.cuda.Stream] = None) -> None:
+    _lib.init()
+    dev = _dev(buf)
+    check("hf_inject_bitflip", _lib.load().hf_inject_bitflip(
+        buf.data_ptr(), hf_dtype(buf), int(elem), int(bit), dev, _stream_ptr(dev, stream)))
+
+
+def inject_scale(buf: torch.Tensor, elem: int, rel: float,
+                 stream: Optional[torch.cuda.Stream] = None) -> None:
+    _lib.init()
+    dev = _dev(buf)
+    check("hf_inject_scale", _lib.load().hf_inject_scale(
+        buf.data_ptr(), hf_dtype(buf), int(elem), float(rel), dev, _stream_ptr(dev, stream)))
+
+
+def scribble(buf: torch.Tensor, data: bytes, stream: Optional[torch.cuda.Stream] = None) -> None:
+    _lib.init()
+    dev = _dev(buf)
+    raw = (ctypes.c_uint8 * max(1, len(data)))(*data)
+    check("hf_scribble", _lib.load().hf_scribble(buf.data_ptr(), raw, len(data), dev,
+                                                 _stream_ptr(dev, stream)))
+
+
+# ---- matmul variants -------------------------------------------------------------
+
+def _mm_args(A: torch.Tensor, B: torch.Tensor, C: torch.Tensor):
+    if A.dtype != torch.float32 or B.dtype != torch.float32 or C.dtype != torch.float32:
+        raise ValueError("matmul variants take fp32 operands")
+    if A.dim() != 2 or B.dim() != 2 or C.dim() != 2:
+        raise ValueError("matmul variants take 2-D operands")
+    M, K = A.shape
+    K2, N = B.shape
+    if K2 != K or tuple(C.shape) != (M, N):
+        raise ValueError(f"shape mismatch {tuple(A.shape)} x {tuple(B.shape)} -> {tuple(C.shape)}")
+    for t in (A, B, C):
+        if not t.is_contiguous():
+            raise ValueError("matmul operands must be contiguous row-major")
+    return M, N, K
+
+
+def gemm_simt(A: torch.Tensor, B: torch.Tensor, C: torch.Tensor,
+              stream: Optional[torch.cuda.Stream] = None) -> None:
+    M, N, K = _mm_args(A, B, C)
+    _lib.init()
+    dev = _dev(C)
+    check("hf_gemm_simt", _lib.load().hf_gemm_simt(A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K,
+                                                   dev, _stream_ptr(dev, stream)))
+
+
+def gemm_tc(A: torch.Tensor, B: torch.Tensor, C: torch.Tensor, mode: int = _lib.HF_GEMM_TF32,
+            stream: Optional[torch.cuda.Stream] = None) -> None:
+    M, N, K = _mm_args(A, B, C)
+    _lib.init()
+    dev = _dev(C)
+    check("hf_gemm_tc", _lib.load().hf_gemm_tc(A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K,
+                                               mode, dev, _stream_ptr(dev, stream)))

@@ -1,0 +1,282 @@
+"""GPU parity of the libhetft kernels against the oracle and the reference
+golden fixtures.  Every call goes through the C-ABI (include/hetft.h).
+
+Bar: voter decisions, counts, winner, first divergence and the voted buffer
+bit-exact; checksums / injections / copies bit-exact; matmul variants within
+the voter tolerance δ = 1e-3 of the binary64 oracle (tolerance stated where
+used)."""
+
+import random
+
+import numpy as np
+import pytest
+
+from golden_io import as_array, inject_golden, voter_cases
+from oracle import checksum as ochecksum
+from oracle import fault_schedule, inject as oinject
+from oracle import matmul as omatmul
+from oracle import vote as ovote
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def K():
+    from paper_1405_2912_b200 import kernels
+    return kernels
+
+
+def dev(a: np.ndarray):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def check_vote(res, ores, voted=None):
+    assert res.verdict == ores.verdict
+    assert res.mismatch == ores.mismatch
+    assert res.unresolved == ores.unresolved
+    assert res.first_div == ores.first_div
+    assert res.winner == ores.winner
+    if voted is not None:
+        got = voted.cpu().numpy()
+        assert got.tobytes() == np.ascontiguousarray(ores.voted).tobytes()
+
+
+CASES = voter_cases()
+
+
+@pytest.mark.parametrize("case", CASES, ids=[f"{c['vt']}{c['width']}-{i}" for i, c in enumerate(CASES)])
+def test_k2_vote_matches_reference_golden(K, case):
+    a = as_array(case["a"], case["vt"], case["width"])
+    b = as_array(case["b"], case["vt"], case["width"])
+    if case["vt"] == "int" and case["width"] not in (1, 2, 4, 8):
+        ta, tb = dev(a), dev(b)
+        voted = torch.empty_like(ta)
+        res = K.vote_bytes([ta, tb], case["width"], voted=voted)
+        ores = ovote.vote_bytes([a, b], case["width"])
+    else:
+        ta, tb = dev(a), dev(b)
+        voted = torch.empty_like(ta)
+        res = K.vote([ta, tb], case["delta"], voted=voted)
+        ores = ovote.vote([a, b], case["delta"])
+    # the reference's own verdict and first divergence (K = 2)
+    assert (res.verdict == "match") == (case["verdict"] == "match")
+    assert res.first_div == case["first_div"]
+    check_vote(res, ores, voted)
+
+
+def _replicas(rng, K, n, dtype, n_faults, mode="bitflip"):
+    if np.dtype(dtype).kind == "f":
+        base = rng.uniform(1, 2, n).astype(dtype)
+    else:
+        base = rng.integers(0, 2 ** 16, n).astype(dtype)
+    reps = [base.copy() for _ in range(K)]
+    width = np.dtype(dtype).itemsize
+    for _ in range(n_faults):
+        r = int(rng.integers(0, K))
+        i = int(rng.integers(0, n))
+        if mode == "bitflip":
+            oinject.bitflip(reps[r], i, int(rng.integers(0, 8 * width)))
+        else:
+            oinject.corrupt_scale(reps[r], i, float(rng.choice([1e-4, 2e-3, 0.5])))
+    return reps
+
+
+@pytest.mark.parametrize("Kr", [2, 3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("dtype", [np.float32, np.float64, np.uint8, np.uint16, np.uint32, np.uint64])
+def test_k_way_vote_parity(K, Kr, dtype):
+    rng = np.random.default_rng(Kr * 131 + np.dtype(dtype).itemsize)
+    for n, faults in ((1, 1), (7, 3), (4096, 0), (100_003, 40)):
+        reps = _replicas(rng, Kr, n, dtype, faults)
+        rel = [float(x) for x in rng.choice([1e-3, 1e-4, 5e-3], Kr)]
+        td = [dev(r) for r in reps]
+        voted = torch.empty_like(td[0])
+        res = K.vote(td, rel, voted=voted)
+        check_vote(res, ovote.vote(reps, rel), voted)
+
+
+def test_vote_ulp_rule(K):
+    rng = np.random.default_rng(5)
+    for dtype in (np.float32, np.float64):
+        a = rng.uniform(-1, 1, 50_000).astype(dtype)
+        b = a.copy()
+        c = a.copy()
+        bits = b.view(np.uint32 if dtype == np.float32 else np.uint64)
+        bits += rng.integers(0, 9, a.size).astype(bits.dtype)  # 0..8 ulps
+        c[::7] = -c[::7]
+        c[3] = np.nan
+        for ulp in ([4, 4, 4], [0, 8, 2], [16, 1, 1]):
+            reps = [a, b, c]
+            res = K.vote([dev(x) for x in reps], [0.0, 0.0, 0.0], ulp_tol=ulp)
+            check_vote(res, ovote.vote(reps, 0.0, ulp_tol=ulp))
+
+
+def test_vote_unaligned_and_tails(K):
+    rng = np.random.default_rng(9)
+    for dtype in (np.float32, np.uint8, np.float64, np.uint16):
+        n = 10_001
+        reps = _replicas(rng, 3, n + 1, dtype, 25)
+        td = [dev(r)[1:] for r in reps]           # offset by one element: not 16B aligned
+        voted = torch.empty(n, dtype=td[0].dtype, device="cuda")
+        res = K.vote(td, 1e-3, voted=voted)
+        check_vote(res, ovote.vote([r[1:] for r in reps], 1e-3), voted)
+
+
+def test_vote_empty_and_errors(K):
+    from paper_1405_2912_b200._lib import HfError
+    e = torch.empty(0, dtype=torch.float32, device="cuda")
+    res = K.vote([e, e, e], 1e-3)
+    assert res.verdict == "match" and res.first_div == -1
+    a = torch.zeros(4, device="cuda")
+    with pytest.raises(ValueError):
+        K.vote([a], 1e-3)
+    with pytest.raises(HfError):
+        K.vote([a, a], -1.0)
+
+
+def test_vote_large_sparse_faults(K):
+    rng = np.random.default_rng(11)
+    n = 1 << 24
+    base = rng.uniform(1, 2, n).astype(np.float32)
+    reps = [base, base.copy(), base.copy()]
+    for r, i, bit in ((1, 5, 30), (2, n - 1, 22), (0, n // 2, 14), (1, n // 2, 3)):
+        oinject.bitflip(reps[r], i, bit)
+    td = [dev(r) for r in reps]
+    voted = torch.empty_like(td[0])
+    res = K.vote(td, 1e-3, voted=voted)
+    check_vote(res, ovote.vote(reps, 1e-3), voted)
+
+
+def test_vote_async_back_to_back(K):
+    rng = np.random.default_rng(3)
+    ws = K.VoteWorkspace(torch.cuda.current_device())
+    for i in range(5):
+        reps = _replicas(rng, 3, 70_000, np.float32, i * 3, mode="scale")
+        td = [dev(r) for r in reps]
+        voted = torch.empty_like(td[0])
+        K.vote_async(td, ws, 1e-3, voted=voted)
+        torch.cuda.synchronize()
+        check_vote(ws.read(), ovote.vote(reps, 1e-3), voted)
+
+
+# ---- checksum / checkpoint / copy ---------------------------------------------
+
+@pytest.mark.parametrize("nbytes", [0, 1, 3, 4, 15, 16, 17, 4096, 1_000_003, 1 << 22])
+def test_checksum_matches_oracle(K, nbytes):
+    rng = np.random.default_rng(nbytes)
+    raw = rng.integers(0, 256, nbytes, dtype=np.uint8)
+    t = dev(raw)
+    assert K.checksum(t) == ochecksum.checksum(raw)
+    if nbytes > 1:
+        # unaligned view exercises the byte path
+        assert K.checksum(t[1:]) == ochecksum.checksum(raw[1:])
+
+
+def test_checksum_position_sensitive(K):
+    a = np.arange(1024, dtype=np.uint32)
+    b = a.copy()
+    b[[3, 9]] = b[[9, 3]]
+    assert K.checksum(dev(a)) != K.checksum(dev(b))
+
+
+def test_checkpoint_restore_roundtrip(K):
+    from paper_1405_2912_b200._lib import HfError
+    rng = np.random.default_rng(2)
+    x = rng.uniform(1, 2, 1_000_001).astype(np.float32)
+    buf = dev(x)
+    ck = torch.empty_like(buf)
+    cs = K.checkpoint(ck, buf, with_checksum=True)
+    assert cs == ochecksum.checksum(x)
+    K.inject_bitflip(buf, 12345, 7)
+    K.restore(buf, ck, expect=cs)
+    torch.cuda.synchronize()
+    assert buf.cpu().numpy().tobytes() == x.tobytes()
+    # a corrupted snapshot is detected on restore
+    K.inject_bitflip(ck, 99, 0)
+    with pytest.raises(HfError):
+        K.restore(buf, ck, expect=cs)
+    # plain checkpoint without checksum
+    ck2 = torch.empty_like(buf)
+    K.checkpoint(ck2, buf)
+    torch.cuda.synchronize()
+    assert torch.equal(ck2, buf)
+
+
+def test_copy_device_and_host(K):
+    x = torch.arange(100_000, dtype=torch.float32, device="cuda")
+    y = torch.empty_like(x)
+    K.copy(y, x)
+    h = torch.empty(100_000, dtype=torch.float32).pin_memory()
+    K.copy(h, x)
+    torch.cuda.synchronize()
+    assert torch.equal(y, x) and torch.equal(h, x.cpu())
+    z = torch.empty_like(x)
+    K.copy(z, h)
+    torch.cuda.synchronize()
+    assert torch.equal(z, x)
+
+
+# ---- injection ------------------------------------------------------------------
+
+_DT = {"f32": np.float32, "f64": np.float64, "u8": np.uint8, "u16": np.uint16,
+       "u32": np.uint32, "u64": np.uint64}
+
+
+@pytest.mark.parametrize("row", inject_golden()["attempts"])
+def test_device_injection_replays_reference(K, row):
+    """Host draws with the reference RNG order; the device applies the fault;
+    the resulting bytes equal what the reference's simulate_execution produced."""
+    dt = _DT[row["kind"]]
+    host = [np.frombuffer(bytes.fromhex(h), dtype=dt).copy() for h in row["before"]]
+    shadow = [h.copy() for h in host]
+    rng = random.Random(row["seed"])
+    ev = fault_schedule.apply_attempt(rng, row["probs"], shadow,
+                                      [row["kind"] in ("f32", "f64")] * len(shadow),
+                                      rel=row["rel"], element=row["element"])
+    tens = [dev(h) for h in host]
+    for vi, vals in ev["scribble"]:
+        w = 1 if row["kind"] in ("f32", "f64") else np.dtype(dt).itemsize
+        data = b"".join(int(v).to_bytes(w, "little") for v in vals)
+        K.scribble(tens[vi], data)
+    if ev["corrupt"] is not None and ev["corrupt"][1] >= 0:
+        which, idx, rel = ev["corrupt"]
+        K.inject_scale(tens[which], idx, rel)
+    torch.cuda.synchronize()
+    assert [t.cpu().numpy().tobytes().hex() for t in tens] == row["after"]
+
+
+def test_bitflip_matches_oracle(K):
+    rng = np.random.default_rng(4)
+    for dtype in (np.float32, np.float64, np.uint8, np.uint16, np.uint32, np.uint64):
+        x = rng.integers(0, 100, 257).astype(dtype)
+        t = dev(x)
+        for _ in range(20):
+            i = int(rng.integers(0, x.size))
+            bit = int(rng.integers(0, 8 * x.itemsize))
+            oinject.bitflip(x, i, bit)
+            K.inject_bitflip(t, i, bit)
+        torch.cuda.synchronize()
+        assert t.cpu().numpy().tobytes() == x.tobytes()
+
+
+# ---- matmul variants ------------------------------------------------------------
+
+def _agree(got: np.ndarray, ref: np.ndarray, delta=1e-3):
+    bad = ovote.reference_first_divergence(got.reshape(-1), ref.reshape(-1), delta)
+    assert bad is None, f"first divergence at {bad}: {got.reshape(-1)[bad]} vs {ref.reshape(-1)[bad]}"
+
+
+@pytest.mark.parametrize("shape", [(128, 128, 16), (256, 384, 64), (1024, 1024, 1024),
+                                   (1, 1, 1), (33, 65, 17), (130, 7, 300)])
+def test_gemm_simt_within_delta(K, shape):
+    M, N, Kd = shape
+    rng = np.random.default_rng(M * N + Kd)
+    a = rng.uniform(1, 2, (M, Kd)).astype(np.float32)
+    b = rng.uniform(1, 2, (Kd, N)).astype(np.float32)
+    c = torch.empty(M, N, dtype=torch.float32, device="cuda")
+    K.gemm_simt(dev(a), dev(b), c)
+    torch.cuda.synchronize()
+    # tolerance: δ = 1e-3 relative (the voter predicate); fp32 FMA accumulation
+    # of U[1,2) products stays ~1e-6 relative of the binary64 oracle
+    _agree(c.cpu().numpy(), omatmul.matmul(a, b))

@@ -1,0 +1,75 @@
+"""Kernel micro-benchmarks (device time via CUDA events).  Not the driver
+bench; used while tuning.  Prints one JSON line per measurement."""
+
+import json
+import sys
+import time
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_1405_2912_b200 import kernels  # noqa: E402
+
+
+def timeit(fn, iters=20, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(iters):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters * 1e-3
+
+
+def main():
+    out = []
+    dev = torch.device("cuda:0")
+    for n in (1 << 20, 1 << 24, 1 << 28):
+        for Kr in (2, 3, 5):
+            reps = [torch.rand(n, device=dev) + 1 for _ in range(Kr)]
+            voted = torch.empty_like(reps[0])
+            ws = kernels.VoteWorkspace(0)
+            t = timeit(lambda: kernels.vote_async(reps, ws, 1e-3, voted=voted))
+            gb = (Kr + 1) * n * 4 / t / 1e9
+            out.append({"k": "vote_f32", "n": n, "K": Kr, "us": t * 1e6, "GBps": gb})
+            print(json.dumps(out[-1]), flush=True)
+            del reps, voted
+        src = torch.rand(n, device=dev)
+        dst = torch.empty_like(src)
+        t = timeit(lambda: kernels.checkpoint(dst, src))
+        out.append({"k": "ckpt", "n": n, "us": t * 1e6, "GBps": 2 * n * 4 / t / 1e9})
+        print(json.dumps(out[-1]), flush=True)
+        t = timeit(lambda: dst.copy_(src))
+        out.append({"k": "torch_copy", "n": n, "us": t * 1e6, "GBps": 2 * n * 4 / t / 1e9})
+        print(json.dumps(out[-1]), flush=True)
+    for N in (1024, 2048, 4096):
+        a = torch.rand(N, N, device=dev) + 1
+        b = torch.rand(N, N, device=dev) + 1
+        c = torch.empty(N, N, device=dev)
+        t = timeit(lambda: kernels.gemm_simt(a, b, c), iters=5)
+        out.append({"k": "gemm_simt", "N": N, "ms": t * 1e3, "TFLOPs": 2 * N ** 3 / t / 1e12})
+        print(json.dumps(out[-1]), flush=True)
+        try:
+            t = timeit(lambda: kernels.gemm_tc(a, b, c), iters=10)
+            out.append({"k": "gemm_tc", "N": N, "ms": t * 1e3, "TFLOPs": 2 * N ** 3 / t / 1e12})
+        except Exception as exc:  # noqa: BLE001
+            out.append({"k": "gemm_tc", "N": N, "error": str(exc)[:200]})
+        print(json.dumps(out[-1]), flush=True)
+        torch.backends.cuda.matmul.allow_tf32 = True
+        t = timeit(lambda: torch.matmul(a, b, out=c), iters=10)
+        out.append({"k": "cublas_tf32", "N": N, "ms": t * 1e3, "TFLOPs": 2 * N ** 3 / t / 1e12})
+        print(json.dumps(out[-1]), flush=True)
+        torch.backends.cuda.matmul.allow_tf32 = False
+        t = timeit(lambda: torch.matmul(a, b, out=c), iters=5)
+        out.append({"k": "cublas_fp32", "N": N, "ms": t * 1e3, "TFLOPs": 2 * N ** 3 / t / 1e12})
+        print(json.dumps(out[-1]), flush=True)
+    Path("gpurun_out").mkdir(exist_ok=True)
+    Path("gpurun_out/microbench.json").write_text(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
