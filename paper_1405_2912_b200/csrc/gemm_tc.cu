@@ -1,7 +1,419 @@
-// hf_gemm_tc: tcgen05 kind::tf32 matmul (placeholder until the tcgen05 kernel lands).
+// hf_gemm_tc: tensor-core fp32 matmul via tcgen05.mma kind::tf32 (sm_100a).
+//
+// The tensor-core half of the diverse kernel pair (§IV-D; attached
+// through the kernel-variant slot of /root/reference/pkg/src/hetrt/api.py:131-138).
+// C = A·B, row-major fp32: A is K-major, B is N-major ("MN-major" UMMA operand).
+//
+// Structure (persistent, warp-specialised, one CTA per SM):
+//   warp 0      TMA producer: A box {32k x 128m} + 8 B boxes {32n x 32k} per
+//               k-block into a 4-stage ring of 128B-swizzled smem (48 KB/stage)
+//   warp 1      MMA issuer: one thread issues 4 x tcgen05.mma (M=128, N=256,
+//               K=8) per k-block into a TMEM accumulator; tcgen05.commit frees
+//               the smem stage and, after the last k-block, signals the epilogue
+//   warp 2      TMEM allocator (2 x 256 columns: double-buffered accumulators)
+//   warps 4..7  epilogue: tcgen05.ld 32x32b.x32 -> registers -> global,
+//               overlapping the next tile's main loop
+// Ragged M/N/K are handled by TMA out-of-bounds zero fill plus masked stores.
+// Mode HF_GEMM_3XTF32 splits each operand into tf32 big + small parts in a
+// pre-pass and runs the same kernel over K' = 3K:
+//   [A_hi | A_hi | A_lo] x [B_hi ; B_lo ; B_hi]  ~= fp32-accurate product.
 #include "common.cuh"
-extern "C" int hf_gemm_tc(const float* A, const float* B, float* C, int M, int N, int K, int mode,
-                          int device, void* stream) {
-    hf::set_error("hf_gemm_tc: not built yet");
-    return HF_EUNSUP;
+
+#include <cuda.h>
+#include <mutex>
+
+namespace hf {
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int BK = 32;          // one 128-byte swizzle row of fp32
+constexpr int UK = 8;           // tf32 UMMA K
+constexpr int STAGES = 4;
+constexpr int A_STAGE = BM * BK * 4;   // 16 KB
+constexpr int B_BOX = 32 * BK * 4;     // 4 KB: 32 n x 32 k
+constexpr int B_STAGE = BN * BK * 4;   // 32 KB
+constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
+constexpr int TMEM_COLS = 512;
+constexpr int NUM_THREADS = 256;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+// ---- PTX wrappers ----------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// tcgen05.ld 32 lanes x 32 bits, 32 consecutive columns per thread
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// UMMA shared-memory descriptor (SM100 "version 1" layout):
+//   [0,14) start>>4  [16,30) LBO>>4  [32,46) SBO>>4  [46,48) version=1
+//   [49,52) base offset  [52] LBO mode  [61,64) layout (2 = SWIZZLE_128B)
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+    d |= 1ull << 46;
+    d |= 2ull << 61;
+    return d;
+}
+
+// Instruction descriptor, kind::tf32, fp32 accumulate, A K-major, B MN-major.
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N) {
+    return (1u << 4)            // D format f32
+           | (2u << 7)          // A format tf32
+           | (2u << 10)         // B format tf32
+           | (0u << 15)         // A K-major
+           | (1u << 16)         // B MN-major
+           | (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+struct Barriers {
+    uint64_t full[STAGES];
+    uint64_t empty[STAGES];
+    uint64_t tmem_full[2];
+    uint64_t tmem_empty[2];
+    uint32_t tmem_base;
+};
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, float* __restrict__ C,
+                 int M, int N, int K) {
+    extern __shared__ uint8_t smem_raw[];
+    // 1024-byte alignment for the SWIZZLE_128B atoms
+    const uint32_t base_u32 = smem_u32(smem_raw);
+    uint8_t* smem = smem_raw + ((1024 - (base_u32 & 1023)) & 1023);
+    Barriers* bars = reinterpret_cast<Barriers*>(smem + STAGES * STAGE_BYTES);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int tiles_m = (M + BM - 1) / BM;
+    const int tiles_n = (N + BN - 1) / BN;
+    const int num_tiles = tiles_m * tiles_n;
+    const int nkb = (K + BK - 1) / BK;
+
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tmA);
+        prefetch_tmap(&tmB);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&bars->full[s], 1);
+            mbar_init(&bars->empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&bars->tmem_full[a], 1);
+            mbar_init(&bars->tmem_empty[a], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&bars->tmem_base)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = bars->tmem_base;
+
+    if (warp == 0) {
+        // ===== TMA producer =====
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                const int tm = tile % tiles_m, tn = tile / tiles_m;
+                const int m0 = tm * BM, n0 = tn * BN;
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(&bars->empty[stage], phase ^ 1);
+                    uint8_t* sa = smem + stage * STAGE_BYTES;
+                    uint8_t* sb = sa + A_STAGE;
+                    mbar_expect_tx(&bars->full[stage], STAGE_BYTES);
+                    tma_load_2d(sa, &tmA, &bars->full[stage], kb * BK, m0);
+#pragma unroll
+                    for (int j = 0; j < BN / 32; ++j)
+                        tma_load_2d(sb + j * B_BOX, &tmB, &bars->full[stage], n0 + 32 * j, kb * BK);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer =====
+        if (lane == 0) {
+            constexpr uint32_t idesc = make_idesc(BM, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int local = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+                const int acc = local & 1;
+                const uint32_t acc_phase = (local >> 1) & 1;
+                mbar_wait(&bars->tmem_empty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem + acc * BN;
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(&bars->full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+                    const uint32_t sb = sa + A_STAGE;
+#pragma unroll
+                    for (int kk = 0; kk < BK / UK; ++kk) {
+                        // A: K-major SW128, advance 32 B along the swizzled row
+                        uint64_t adesc = make_desc(sa + kk * UK * 4, 16, 1024);
+                        // B: MN-major SW128, 8 k-rows (1 KB) per MMA; LBO = 4 KB
+                        // between 32-column boxes, SBO = 1 KB between 8-row groups
+                        uint64_t bdesc = make_desc(sb + kk * UK * 128, B_BOX, 1024);
+                        tc_mma_tf32(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0);
+                    }
+                    tc_commit(&bars->empty[stage]);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                tc_commit(&bars->tmem_full[acc]);
+            }
+        }
+    } else if (warp >= 4) {
+        // ===== epilogue: TMEM -> registers -> global =====
+        const int ew = warp - 4;                 // TMEM lane quarter
+        const int row_in_tile = ew * 32 + lane;
+        int local = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+            const int tm = tile % tiles_m, tn = tile / tiles_m;
+            const int m0 = tm * BM, n0 = tn * BN;
+            const int acc = local & 1;
+            mbar_wait(&bars->tmem_full[acc], (local >> 1) & 1);
+            tc_fence_after();
+            const int row = m0 + row_in_tile;
+            const uint32_t tbase = tmem + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
+            float* crow = C + static_cast<long long>(row) * N;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                float v[32];
+                tmem_ld32(tbase + c * 32, v);
+                const int col0 = n0 + c * 32;
+                if (row < M) {
+                    if (col0 + 32 <= N && (N & 3) == 0) {
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            *reinterpret_cast<float4*>(crow + col0 + 4 * q) =
+                                make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                    } else {
+                        for (int q = 0; q < 32; ++q)
+                            if (col0 + q < N) crow[col0 + q] = v[q];
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars->tmem_empty[acc]);
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    }
+}
+
+// 3xTF32 pre-pass: hi = tf32(x) (round to nearest, low 13 bits cleared),
+// lo = tf32(x - hi).  Writes A3 = [A_hi | A_hi | A_lo] (M x 3K) and
+// B3 = [B_hi ; B_lo ; B_hi] (3K x N).
+__device__ __forceinline__ float to_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+__global__ void split3_a(const float* __restrict__ A, float* __restrict__ A3, int M, int K) {
+    long long total = static_cast<long long>(M) * K;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        long long m = i / K, k = i % K;
+        float x = A[i];
+        float hi = to_tf32(x);
+        float lo = to_tf32(x - hi);
+        float* row = A3 + m * 3LL * K;
+        row[k] = hi;
+        row[K + k] = hi;
+        row[2LL * K + k] = lo;
+    }
+}
+
+__global__ void split3_b(const float* __restrict__ B, float* __restrict__ B3, int K, int N) {
+    long long total = static_cast<long long>(K) * N;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        float x = B[i];
+        float hi = to_tf32(x);
+        float lo = to_tf32(x - hi);
+        B3[i] = hi;
+        B3[static_cast<long long>(K) * N + i] = lo;
+        B3[2LL * K * N + i] = hi;
+    }
+}
+
+// ---- host side ----------------------------------------------------------------
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeFn get_encode() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    });
+    return fn;
+}
+
+static int make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
+                    uint32_t box_inner, uint32_t box_outer) {
+    EncodeFn enc = get_encode();
+    if (!enc) {
+        set_error("hf_gemm_tc: cuTensorMapEncodeTiled unavailable");
+        return HF_ECUDA;
+    }
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {row_bytes};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("hf_gemm_tc: cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+        return HF_ECUDA;
+    }
+    return HF_OK;
+}
+
+static int launch(const float* A, const float* B, float* C, int M, int N, int K, int device, cudaStream_t st) {
+    CUtensorMap ta, tb;
+    int rc = make_map(&ta, A, static_cast<uint64_t>(K), static_cast<uint64_t>(M), static_cast<uint64_t>(K) * 4, BK, BM);
+    if (rc) return rc;
+    rc = make_map(&tb, B, static_cast<uint64_t>(N), static_cast<uint64_t>(K), static_cast<uint64_t>(N) * 4, 32, BK);
+    if (rc) return rc;
+    static bool attr_set[64] = {false};
+    if (!attr_set[device]) {
+        HF_CUDA_CHECK(cudaFuncSetAttribute(gemm_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+        attr_set[device] = true;
+    }
+    const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+    const int sms = num_sms(device);
+    const int grid = tiles < sms ? tiles : sms;
+    gemm_tf32_kernel<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ta, tb, C, M, N, K);
+    HF_CHECK_LAUNCH();
+    return HF_OK;
+}
+
+}  // namespace tc
+}  // namespace hf
+
+extern "C" int hf_gemm_tc(const float* A, const float* B, float* C, int M, int N, int K, int mode, int device,
+                          void* stream) {
+    HF_REQUIRE(A && B && C, "hf_gemm_tc: NULL operand");
+    HF_REQUIRE(M > 0 && N > 0 && K > 0, "hf_gemm_tc: bad shape %dx%dx%d", M, N, K);
+    HF_REQUIRE(mode == HF_GEMM_TF32 || mode == HF_GEMM_3XTF32, "hf_gemm_tc: unknown mode %d", mode);
+    if (K % 4 != 0 || N % 4 != 0 || (reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) % 16 != 0) {
+        hf::set_error("hf_gemm_tc: TMA needs 16-byte aligned operands and K %% 4 == N %% 4 == 0 (got K=%d N=%d)", K, N);
+        return HF_EUNSUP;
+    }
+    hf::DeviceGuard g(device);
+    HF_REQUIRE(g.ok, "hf_gemm_tc: cannot select device %d", device);
+    cudaStream_t st = hf::as_stream(stream);
+    if (mode == HF_GEMM_TF32) return hf::tc::launch(A, B, C, M, N, K, device, st);
+    // 3xTF32: split into hi/lo planes in scratch, then one tf32 GEMM over 3K
+    float *A3 = nullptr, *B3 = nullptr;
+    size_t a3 = static_cast<size_t>(M) * 3 * K * sizeof(float), b3 = static_cast<size_t>(K) * 3 * N * sizeof(float);
+    HF_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&A3), a3, st));
+    HF_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&B3), b3, st));
+    int grid = hf::num_sms(device) * 8;
+    hf::tc::split3_a<<<grid, 256, 0, st>>>(A, A3, M, K);
+    hf::tc::split3_b<<<grid, 256, 0, st>>>(B, B3, K, N);
+    HF_CHECK_LAUNCH();
+    int rc = hf::tc::launch(A3, B3, C, M, N, 3 * K, device, st);
+    cudaFreeAsync(A3, st);
+    cudaFreeAsync(B3, st);
+    return rc;
 }

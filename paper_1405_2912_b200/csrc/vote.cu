@@ -44,6 +44,8 @@ struct VoteParams {
     int64_t n;      // elements
     int64_t nvec;   // 16-byte vectors handled by the vector loop
     double pdelta[kMaxPairs];   // max(δ_r, δ_s) per pair (r<s)
+    float pdl[kMaxPairs];       // fp32 screen bounds (see Elem<HF_F32>)
+    float pdh[kMaxPairs];
     long long pulp[kMaxPairs];  // max(u_r, u_s) per pair, < 0 = ULP rule off
     hf_vote_result* out;
     VoteWorkspace* ws;
@@ -99,14 +101,31 @@ __device__ __forceinline__ bool ulp_ok64(uint64_t a, uint64_t b, long long u) {
 template <int DT>
 struct Elem;
 
+// fp32 pairs: an exact single-precision screen decides almost every pair;
+// only ambiguous, non-finite, overflowing or subnormal cases take the
+// binary64 path.  With d = RN32(|a-b|), m = max(|a|,|b|) and the host-side
+// constants dl = RN32(RN32(δ)(1-2^-18)), dh = RN32(RN32(δ)(1+2^-18)):
+//   d <= RN32(dl*m)  =>  |a-b| < δm(1-2^-19)          => reference accepts
+//   d >= RN32(dh*m)  =>  |a-b| > δm(1+2^-19)          => reference rejects
+// (each RN32 step is within 2^-24 relative when its result is a finite
+// normal number, which the guard checks; binary64 rounding of |a-b| and δm
+// moves them by 2^-53 only, so neither decision can flip).
 template <>
 struct Elem<HF_F32> {
     using T = uint32_t;
     static constexpr int kPerVec = 4;
-    __device__ static __forceinline__ bool ok(T a, T b, double delta, long long ulp) {
+    __device__ static __forceinline__ bool ok(T a, T b, double delta, float dl, float dh, long long ulp) {
         if (a == b) return true;  // bit-identical (incl. identical NaN payloads)
-        bool r = rel_ok(static_cast<double>(__uint_as_float(a)),
-                        static_cast<double>(__uint_as_float(b)), delta);
+        const float fa = __uint_as_float(a), fb = __uint_as_float(b);
+        const float d = fabsf(fa - fb);
+        const float m = fmaxf(fabsf(fa), fabsf(fb));
+        const float tl = dl * m, th = dh * m;
+        bool r;
+        if (d < INFINITY && th < INFINITY && tl >= 1.17549435e-38f && !(d > tl && d < th)) {
+            r = d <= tl;
+        } else {
+            r = rel_ok(static_cast<double>(fa), static_cast<double>(fb), delta);
+        }
         if (!r && ulp >= 0) r = ulp_ok32(a, b, ulp);
         return r;
     }
@@ -116,7 +135,7 @@ template <>
 struct Elem<HF_F64> {
     using T = uint64_t;
     static constexpr int kPerVec = 2;
-    __device__ static __forceinline__ bool ok(T a, T b, double delta, long long ulp) {
+    __device__ static __forceinline__ bool ok(T a, T b, double delta, float, float, long long ulp) {
         if (a == b) return true;
         bool r = rel_ok(__longlong_as_double(static_cast<long long>(a)),
                         __longlong_as_double(static_cast<long long>(b)), delta);
@@ -129,7 +148,7 @@ template <typename U, int PV>
 struct IntElem {
     using T = U;
     static constexpr int kPerVec = PV;
-    __device__ static __forceinline__ bool ok(T a, T b, double, long long) { return a == b; }
+    __device__ static __forceinline__ bool ok(T a, T b, double, float, float, long long) { return a == b; }
 };
 template <> struct Elem<HF_U8> : IntElem<uint8_t, 16> {};
 template <> struct Elem<HF_U16> : IntElem<uint16_t, 8> {};
@@ -166,25 +185,28 @@ __device__ __forceinline__ typename Elem<DT>::T vote_elem(const typename Elem<DT
                                                            const VoteParams& p, Acc<K>& acc,
                                                            unsigned long long idx) {
     using E = Elem<DT>;
+    // Lazy pair evaluation in replica order: when replica r is evaluated all
+    // its pairs are known (pairs (r', r) for r' < r were computed earlier), so
+    // the first r reaching a majority is v(i).  When every replica agrees this
+    // costs K-1 pair predicates instead of K(K-1)/2.
     uint32_t agree[K];
 #pragma unroll
     for (int r = 0; r < K; ++r) agree[r] = 1u << r;
-#pragma unroll
-    for (int r = 0; r < K; ++r) {
-#pragma unroll
-        for (int s = r + 1; s < K; ++s) {
-            const int pi = pair_index<K>(r, s);
-            if (E::ok(x[r], x[s], p.pdelta[pi], p.pulp[pi])) {
-                agree[r] |= 1u << s;
-                agree[s] |= 1u << r;
-            }
-        }
-    }
     int v = -1;
 #pragma unroll
-    for (int r = K - 1; r >= 0; --r) {
-        // 2*(agree_r + 1) > K with agree_r counted without self
-        if (2 * __popc(agree[r]) > K) v = r;
+    for (int r = 0; r < K; ++r) {
+        if (v < 0) {
+#pragma unroll
+            for (int s = r + 1; s < K; ++s) {
+                const int pi = pair_index<K>(r, s);
+                if (E::ok(x[r], x[s], p.pdelta[pi], p.pdl[pi], p.pdh[pi], p.pulp[pi])) {
+                    agree[r] |= 1u << s;
+                    agree[s] |= 1u << r;
+                }
+            }
+            // 2*(agree_r + 1) > K with agree_r counted without self
+            if (2 * __popc(agree[r]) > K) v = r;
+        }
     }
     typename E::T out = x[0];
     bool flag;
@@ -530,7 +552,8 @@ static int fill_params(VoteParams& p, const void* const* replicas, int K, int64_
     bool aligned = (voted == nullptr) || (reinterpret_cast<uintptr_t>(voted) % 16 == 0);
     for (int r = 0; r < K; ++r) {
         HF_REQUIRE(replicas[r] != nullptr || n == 0, "hf_vote: replica %d is NULL", r);
-        HF_REQUIRE(reinterpret_cast<uintptr_t>(replicas[r]) % (width > 8 ? 1 : width) == 0,
+        const int align = (width == 1 || width == 2 || width == 4 || width == 8) ? width : 1;
+        HF_REQUIRE(reinterpret_cast<uintptr_t>(replicas[r]) % align == 0,
                    "hf_vote: replica %d not aligned to its element size", r);
         p.rep[r] = static_cast<const uint8_t*>(replicas[r]);
         aligned &= reinterpret_cast<uintptr_t>(replicas[r]) % 16 == 0;
@@ -545,6 +568,16 @@ static int fill_params(VoteParams& p, const void* const* replicas, int K, int64_
             double dr = rel_tol ? rel_tol[r] : 0.0, ds = rel_tol ? rel_tol[s] : 0.0;
             HF_REQUIRE(!(dr < 0) && !(ds < 0), "hf_vote: negative relative tolerance");
             p.pdelta[pi] = dr > ds ? dr : ds;
+            {
+                const float d32 = static_cast<float>(p.pdelta[pi]);   // RN
+                if (d32 >= 0x1p-100f && d32 <= 0x1p100f) {
+                    p.pdl[pi] = d32 * (1.0f - 0x1p-18f);
+                    p.pdh[pi] = d32 * (1.0f + 0x1p-18f);
+                } else {  // tiny/huge δ: screen disabled, binary64 decides
+                    p.pdl[pi] = -1.0f;
+                    p.pdh[pi] = -1.0f;
+                }
+            }
             if (ulp_tol) {
                 long long ur = ulp_tol[r], us = ulp_tol[s];
                 p.pulp[pi] = ur > us ? ur : us;
