@@ -280,3 +280,38 @@ def test_gemm_simt_within_delta(K, shape):
     # tolerance: δ = 1e-3 relative (the voter predicate); fp32 FMA accumulation
     # of U[1,2) products stays ~1e-6 relative of the binary64 oracle
     _agree(c.cpu().numpy(), omatmul.matmul(a, b))
+
+
+@pytest.mark.parametrize("shape", [(128, 256, 32), (256, 512, 64), (1024, 1024, 1024),
+                                   (2048, 2048, 2048), (200, 100, 36), (384, 136, 4100)])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_gemm_tc_within_delta(K, shape, mode):
+    M, N, Kd = shape
+    rng = np.random.default_rng(M + 7 * N + Kd + mode)
+    a = rng.uniform(1, 2, (M, Kd)).astype(np.float32)
+    b = rng.uniform(1, 2, (Kd, N)).astype(np.float32)
+    c = torch.full((M, N), float("nan"), dtype=torch.float32, device="cuda")
+    K.gemm_tc(dev(a), dev(b), c, mode=mode)
+    torch.cuda.synchronize()
+    got = c.cpu().numpy()
+    ref = omatmul.matmul(a, b)
+    # tolerance: δ = 1e-3 (voter predicate) for single-pass tf32 on U[1,2)
+    # operands; 3xTF32 (mode 1) must reach 1e-5
+    _agree(got, ref, 1e-3 if mode == 0 else 1e-5)
+
+
+def test_gemm_tc_general_signs(K):
+    """N(0,1) operands: |err| <= 2^-9 * (|A|·|B|) elementwise (tf32 keeps 10
+    mantissa bits per operand; fp32 accumulation)."""
+    rng = np.random.default_rng(77)
+    M = N = 512
+    Kd = 256
+    a = rng.standard_normal((M, Kd)).astype(np.float32)
+    b = rng.standard_normal((Kd, N)).astype(np.float32)
+    c = torch.empty(M, N, dtype=torch.float32, device="cuda")
+    K.gemm_tc(dev(a), dev(b), c)
+    torch.cuda.synchronize()
+    ref = a.astype(np.float64) @ b.astype(np.float64)
+    scale = np.abs(a).astype(np.float64) @ np.abs(b).astype(np.float64)
+    err = np.abs(c.cpu().numpy() - ref)
+    assert np.all(err <= 2.0 ** -9 * scale + 1e-6)
