@@ -6,19 +6,23 @@
 // tensor cores, accumulates every output in fp32 in ascending k order with
 // fused multiply-add, and so fails independently of the tcgen05 variant.
 //
-// Fast path (M%128 == N%128 == 0, K%16 == 0, 16B-aligned): 128x128x16 CTA
+// Fast path (M%128 == N%128 == 0, K%8 == 0, 16B-aligned): 128x128x8 CTA
 // tile, 256 threads, 8x8 outputs per thread as 2x2 blocks of 4x4, A staged
 // transposed in shared memory, two smem stages with a register prefetch of the
-// next k-tile, one barrier per k-tile.  Warps are laid out 4x2 over the
+// next k-tile, one barrier per k-tile, register double-buffered fragments.  Warps are laid out 4x2 over the
 // 16x16 thread grid so each LDS.128 of A and of B is one wavefront.
 // Generic path: 16x16 bounds-checked tiles for ragged shapes.
 #include "common.cuh"
 
 namespace hf {
 
-constexpr int SB_M = 128, SB_N = 128, SB_K = 16, S_PAD = 4;
+constexpr int SB_M = 128, SB_N = 128, SB_K = 8, S_PAD = 4;
 
-__global__ void __launch_bounds__(256, 1)
+// 128x128x8 CTA tile, 256 threads, 8x8 per thread; fragments for k+1 are
+// loaded from shared memory while k is multiplied (register double buffer),
+// the next k-tile is prefetched from global into registers; <= 128 registers
+// so two CTAs (16 warps) share an SM.
+__global__ void __launch_bounds__(256, 2)
 sgemm_128x128(const float* __restrict__ A, const float* __restrict__ B, float* __restrict__ C,
               int M, int N, int K) {
     __shared__ __align__(16) float As[2][SB_K][SB_M + S_PAD];
@@ -33,40 +37,20 @@ sgemm_128x128(const float* __restrict__ A, const float* __restrict__ B, float* _
     const int tiles_n = N / SB_N;
     const int tiles_m = M / SB_M;
     const int group = 8;
-    int bid = blockIdx.x;
-    int per_group = group * tiles_n;
-    int g = bid / per_group;
-    int first_m = g * group;
-    int gm = min(tiles_m - first_m, group);
-    int tm = first_m + (bid % per_group) % gm;
-    int tn = (bid % per_group) / gm;
+    const int bid = blockIdx.x;
+    const int per_group = group * tiles_n;
+    const int g = bid / per_group;
+    const int first_m = g * group;
+    const int gm = min(tiles_m - first_m, group);
+    const int tm = first_m + (bid % per_group) % gm;
+    const int tn = (bid % per_group) / gm;
     const int m0 = tm * SB_M, n0 = tn * SB_N;
 
-    // global->smem load mapping
-    const int a_row = t & 127, a_kh = (t >> 7) * 8;    // A: row, k-half (0 or 8)
-    const int b_k = t >> 5, b_n4 = (t & 31) * 4;        // B: k rows b_k and b_k+8
-    const float* Ag = A + static_cast<long long>(m0 + a_row) * K + a_kh;
-    const float* Bg = B + static_cast<long long>(b_k) * N + n0 + b_n4;
-
-    float4 ra0, ra1, rb0, rb1;
-    auto gload = [&](int k0) {
-        ra0 = __ldg(reinterpret_cast<const float4*>(Ag + k0));
-        ra1 = __ldg(reinterpret_cast<const float4*>(Ag + k0 + 4));
-        rb0 = __ldg(reinterpret_cast<const float4*>(Bg + static_cast<long long>(k0) * N));
-        rb1 = __ldg(reinterpret_cast<const float4*>(Bg + static_cast<long long>(k0 + 8) * N));
-    };
-    auto sstore = [&](int s) {
-        As[s][a_kh + 0][a_row] = ra0.x;
-        As[s][a_kh + 1][a_row] = ra0.y;
-        As[s][a_kh + 2][a_row] = ra0.z;
-        As[s][a_kh + 3][a_row] = ra0.w;
-        As[s][a_kh + 4][a_row] = ra1.x;
-        As[s][a_kh + 5][a_row] = ra1.y;
-        As[s][a_kh + 6][a_row] = ra1.z;
-        As[s][a_kh + 7][a_row] = ra1.w;
-        *reinterpret_cast<float4*>(&Bs[s][b_k][b_n4]) = rb0;
-        *reinterpret_cast<float4*>(&Bs[s][b_k + 8][b_n4]) = rb1;
-    };
+    // global->smem mapping: A 128x8 (one float4 per thread), B 8x128 (one float4)
+    const int a_row = t >> 1, a_k = (t & 1) * 4;
+    const int b_k = t >> 5, b_n = (t & 31) * 4;
+    const float* Ag = A + static_cast<long long>(m0 + a_row) * K + a_k;
+    const float* Bg = B + static_cast<long long>(b_k) * N + n0 + b_n;
 
     float acc[8][8];
 #pragma unroll
@@ -74,31 +58,59 @@ sgemm_128x128(const float* __restrict__ A, const float* __restrict__ B, float* _
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
 
-    gload(0);
-    sstore(0);
+    float4 ra = __ldg(reinterpret_cast<const float4*>(Ag));
+    float4 rb = __ldg(reinterpret_cast<const float4*>(Bg));
+    As[0][a_k + 0][a_row] = ra.x;
+    As[0][a_k + 1][a_row] = ra.y;
+    As[0][a_k + 2][a_row] = ra.z;
+    As[0][a_k + 3][a_row] = ra.w;
+    *reinterpret_cast<float4*>(&Bs[0][b_k][b_n]) = rb;
     __syncthreads();
+
+    float4 fa[2][2], fb[2][2];
+    fa[0][0] = *reinterpret_cast<const float4*>(&As[0][0][ty * 4]);
+    fa[0][1] = *reinterpret_cast<const float4*>(&As[0][0][64 + ty * 4]);
+    fb[0][0] = *reinterpret_cast<const float4*>(&Bs[0][0][tx * 4]);
+    fb[0][1] = *reinterpret_cast<const float4*>(&Bs[0][0][64 + tx * 4]);
 
     const int nk = K / SB_K;
     for (int kt = 0; kt < nk; ++kt) {
         const int s = kt & 1;
-        if (kt + 1 < nk) gload((kt + 1) * SB_K);
+        const bool more = kt + 1 < nk;
+        if (more) {
+            ra = __ldg(reinterpret_cast<const float4*>(Ag + (kt + 1) * SB_K));
+            rb = __ldg(reinterpret_cast<const float4*>(Bg + static_cast<long long>((kt + 1) * SB_K) * N));
+        }
 #pragma unroll
         for (int k = 0; k < SB_K; ++k) {
-            float4 a0 = *reinterpret_cast<const float4*>(&As[s][k][ty * 4]);
-            float4 a1 = *reinterpret_cast<const float4*>(&As[s][k][64 + ty * 4]);
-            float4 b0 = *reinterpret_cast<const float4*>(&Bs[s][k][tx * 4]);
-            float4 b1 = *reinterpret_cast<const float4*>(&Bs[s][k][64 + tx * 4]);
-            const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-            const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+            const int cur = k & 1, nxt = cur ^ 1;
+            if (k + 1 < SB_K) {
+                fa[nxt][0] = *reinterpret_cast<const float4*>(&As[s][k + 1][ty * 4]);
+                fa[nxt][1] = *reinterpret_cast<const float4*>(&As[s][k + 1][64 + ty * 4]);
+                fb[nxt][0] = *reinterpret_cast<const float4*>(&Bs[s][k + 1][tx * 4]);
+                fb[nxt][1] = *reinterpret_cast<const float4*>(&Bs[s][k + 1][64 + tx * 4]);
+            } else if (more) {
+                // stage the prefetched tile, then start the next tile's fragments
+                As[s ^ 1][a_k + 0][a_row] = ra.x;
+                As[s ^ 1][a_k + 1][a_row] = ra.y;
+                As[s ^ 1][a_k + 2][a_row] = ra.z;
+                As[s ^ 1][a_k + 3][a_row] = ra.w;
+                *reinterpret_cast<float4*>(&Bs[s ^ 1][b_k][b_n]) = rb;
+                __syncthreads();
+                fa[nxt][0] = *reinterpret_cast<const float4*>(&As[s ^ 1][0][ty * 4]);
+                fa[nxt][1] = *reinterpret_cast<const float4*>(&As[s ^ 1][0][64 + ty * 4]);
+                fb[nxt][0] = *reinterpret_cast<const float4*>(&Bs[s ^ 1][0][tx * 4]);
+                fb[nxt][1] = *reinterpret_cast<const float4*>(&Bs[s ^ 1][0][64 + tx * 4]);
+            }
+            const float a[8] = {fa[cur][0].x, fa[cur][0].y, fa[cur][0].z, fa[cur][0].w,
+                                fa[cur][1].x, fa[cur][1].y, fa[cur][1].z, fa[cur][1].w};
+            const float b[8] = {fb[cur][0].x, fb[cur][0].y, fb[cur][0].z, fb[cur][0].w,
+                                fb[cur][1].x, fb[cur][1].y, fb[cur][1].z, fb[cur][1].w};
 #pragma unroll
             for (int i = 0; i < 8; ++i)
 #pragma unroll
                 for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
         }
-        if (kt + 1 < nk) {
-            sstore(s ^ 1);
-        }
-        __syncthreads();
     }
 
 #pragma unroll

@@ -2,10 +2,14 @@
 //
 // The tensor-core half of the diverse kernel pair (§IV-D; attached
 // through the kernel-variant slot of /root/reference/pkg/src/hetrt/api.py:131-138).
-// C = A·B, row-major fp32: A is K-major, B is N-major ("MN-major" UMMA operand).
+// C = A·B, row-major fp32.  Both UMMA operands are K-major: tcgen05 kind::tf32
+// executes MN-major (transposed) smem operands as a no-op on this part
+// (tools/tc_probe.cu, variants v0/v8-v11), so B is first transposed to
+// B^T (N x K) by a tiled pre-pass (~2·|B| bytes of HBM traffic, a few % of
+// the GEMM), fused with the hi/lo split in 3xTF32 mode.
 //
 // Structure (persistent, warp-specialised, one CTA per SM):
-//   warp 0      TMA producer: A box {32k x 128m} + 8 B boxes {32n x 32k} per
+//   warp 0      TMA producer: A box {32k x 128m} + B^T box {32k x 256n} per
 //               k-block into a 4-stage ring of 128B-swizzled smem (48 KB/stage)
 //   warp 1      MMA issuer: one thread issues 4 x tcgen05.mma (M=128, N=256,
 //               K=8) per k-block into a TMEM accumulator; tcgen05.commit frees
@@ -14,7 +18,7 @@
 //   warps 4..7  epilogue: tcgen05.ld 32x32b.x32 -> registers -> global,
 //               overlapping the next tile's main loop
 // Ragged M/N/K are handled by TMA out-of-bounds zero fill plus masked stores.
-// Mode HF_GEMM_3XTF32 splits each operand into tf32 big + small parts in a
+// Mode HF_GEMM_3XTF32 splits each operand into tf32 big + small parts in the
 // pre-pass and runs the same kernel over K' = 3K:
 //   [A_hi | A_hi | A_lo] x [B_hi ; B_lo ; B_hi]  ~= fp32-accurate product.
 #include "common.cuh"
@@ -31,7 +35,6 @@ constexpr int BK = 32;          // one 128-byte swizzle row of fp32
 constexpr int UK = 8;           // tf32 UMMA K
 constexpr int STAGES = 4;
 constexpr int A_STAGE = BM * BK * 4;   // 16 KB
-constexpr int B_BOX = 32 * BK * 4;     // 4 KB: 32 n x 32 k
 constexpr int B_STAGE = BN * BK * 4;   // 32 KB
 constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
 constexpr int TMEM_COLS = 512;
@@ -128,13 +131,13 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
     return d;
 }
 
-// Instruction descriptor, kind::tf32, fp32 accumulate, A K-major, B MN-major.
+// Instruction descriptor, kind::tf32, fp32 accumulate, A and B K-major.
 __host__ __device__ constexpr uint32_t make_idesc(int M, int N) {
     return (1u << 4)            // D format f32
            | (2u << 7)          // A format tf32
            | (2u << 10)         // B format tf32
            | (0u << 15)         // A K-major
-           | (1u << 16)         // B MN-major
+           | (0u << 16)         // B K-major (B^T staged by the pre-pass)
            | (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
 }
 
@@ -200,9 +203,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     uint8_t* sb = sa + A_STAGE;
                     mbar_expect_tx(&bars->full[stage], STAGE_BYTES);
                     tma_load_2d(sa, &tmA, &bars->full[stage], kb * BK, m0);
-#pragma unroll
-                    for (int j = 0; j < BN / 32; ++j)
-                        tma_load_2d(sb + j * B_BOX, &tmB, &bars->full[stage], n0 + 32 * j, kb * BK);
+                    tma_load_2d(sb, &tmB, &bars->full[stage], kb * BK, n0);
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -230,11 +231,10 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     const uint32_t sb = sa + A_STAGE;
 #pragma unroll
                     for (int kk = 0; kk < BK / UK; ++kk) {
-                        // A: K-major SW128, advance 32 B along the swizzled row
+                        // K-major SW128: advance 32 B along the swizzled 128 B row;
+                        // SBO = 1 KB between 8-row groups (LBO unused when swizzled)
                         uint64_t adesc = make_desc(sa + kk * UK * 4, 16, 1024);
-                        // B: MN-major SW128, 8 k-rows (1 KB) per MMA; LBO = 4 KB
-                        // between 32-column boxes, SBO = 1 KB between 8-row groups
-                        uint64_t bdesc = make_desc(sb + kk * UK * 128, B_BOX, 1024);
+                        uint64_t bdesc = make_desc(sb + kk * UK * 4, 16, 1024);
                         tc_mma_tf32(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0);
                     }
                     tc_commit(&bars->empty[stage]);
@@ -291,13 +291,46 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     }
 }
 
-// 3xTF32 pre-pass: hi = tf32(x) (round to nearest, low 13 bits cleared),
-// lo = tf32(x - hi).  Writes A3 = [A_hi | A_hi | A_lo] (M x 3K) and
-// B3 = [B_hi ; B_lo ; B_hi] (3K x N).
+// Pre-pass.  transpose: Bt[n][k] = B[k][n] (bit copy).  3xTF32: hi = tf32(x)
+// (cvt.rna), lo = tf32(x - hi); A3 = [A_hi | A_hi | A_lo] (M x 3K) and
+// Bt3 = [B_hi^T | B_lo^T | B_hi^T] (N x 3K), so one tf32 GEMM over 3K sums
+// A_hi·B_hi + A_hi·B_lo + A_lo·B_hi.  32x32 tiles through padded smem keep
+// both the read and the write coalesced.
 __device__ __forceinline__ float to_tf32(float x) {
     uint32_t r;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
     return __uint_as_float(r);
+}
+
+template <bool kSplit>
+__global__ void __launch_bounds__(256) transpose_b(const float* __restrict__ B, float* __restrict__ Bt, int K, int N) {
+    __shared__ float tile[32][33];
+    const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+#pragma unroll
+    for (int r = ty; r < 32; r += 8) {
+        const int k = k0 + r, n = n0 + tx;
+        tile[r][tx] = (k < K && n < N) ? B[static_cast<long long>(k) * N + n] : 0.f;
+    }
+    __syncthreads();
+    const long long ld = kSplit ? 3LL * K : K;
+#pragma unroll
+    for (int r = ty; r < 32; r += 8) {
+        const int n = n0 + r, k = k0 + tx;
+        if (n < N && k < K) {
+            const float x = tile[tx][r];
+            float* row = Bt + static_cast<long long>(n) * ld;
+            if (kSplit) {
+                const float hi = to_tf32(x);
+                const float lo = to_tf32(x - hi);
+                row[k] = hi;
+                row[K + k] = lo;
+                row[2LL * K + k] = hi;
+            } else {
+                row[k] = x;
+            }
+        }
+    }
 }
 
 __global__ void split3_a(const float* __restrict__ A, float* __restrict__ A3, int M, int K) {
@@ -312,19 +345,6 @@ __global__ void split3_a(const float* __restrict__ A, float* __restrict__ A3, in
         row[k] = hi;
         row[K + k] = hi;
         row[2LL * K + k] = lo;
-    }
-}
-
-__global__ void split3_b(const float* __restrict__ B, float* __restrict__ B3, int K, int N) {
-    long long total = static_cast<long long>(K) * N;
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-         i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        float x = B[i];
-        float hi = to_tf32(x);
-        float lo = to_tf32(x - hi);
-        B3[i] = hi;
-        B3[static_cast<long long>(K) * N + i] = lo;
-        B3[2LL * K * N + i] = hi;
     }
 }
 
@@ -368,11 +388,12 @@ static int make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t
     return HF_OK;
 }
 
-static int launch(const float* A, const float* B, float* C, int M, int N, int K, int device, cudaStream_t st) {
+// A: M x K row-major, Bt: N x K row-major (both K-major)
+static int launch(const float* A, const float* Bt, float* C, int M, int N, int K, int device, cudaStream_t st) {
     CUtensorMap ta, tb;
     int rc = make_map(&ta, A, static_cast<uint64_t>(K), static_cast<uint64_t>(M), static_cast<uint64_t>(K) * 4, BK, BM);
     if (rc) return rc;
-    rc = make_map(&tb, B, static_cast<uint64_t>(N), static_cast<uint64_t>(K), static_cast<uint64_t>(N) * 4, 32, BK);
+    rc = make_map(&tb, Bt, static_cast<uint64_t>(K), static_cast<uint64_t>(N), static_cast<uint64_t>(K) * 4, BK, BN);
     if (rc) return rc;
     static bool attr_set[64] = {false};
     if (!attr_set[device]) {
@@ -402,18 +423,31 @@ extern "C" int hf_gemm_tc(const float* A, const float* B, float* C, int M, int N
     hf::DeviceGuard g(device);
     HF_REQUIRE(g.ok, "hf_gemm_tc: cannot select device %d", device);
     cudaStream_t st = hf::as_stream(stream);
-    if (mode == HF_GEMM_TF32) return hf::tc::launch(A, B, C, M, N, K, device, st);
-    // 3xTF32: split into hi/lo planes in scratch, then one tf32 GEMM over 3K
-    float *A3 = nullptr, *B3 = nullptr;
-    size_t a3 = static_cast<size_t>(M) * 3 * K * sizeof(float), b3 = static_cast<size_t>(K) * 3 * N * sizeof(float);
-    HF_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&A3), a3, st));
-    HF_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&B3), b3, st));
-    int grid = hf::num_sms(device) * 8;
-    hf::tc::split3_a<<<grid, 256, 0, st>>>(A, A3, M, K);
-    hf::tc::split3_b<<<grid, 256, 0, st>>>(B, B3, K, N);
+    static bool pool_cfg[64] = {false};
+    if (!pool_cfg[device]) {  // keep stream-ordered scratch cached between calls
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        pool_cfg[device] = true;
+    }
+    const bool split = mode == HF_GEMM_3XTF32;
+    const int Ke = split ? 3 * K : K;
+    float* Bt = nullptr;
+    float* A3 = nullptr;
+    HF_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&Bt), static_cast<size_t>(N) * Ke * sizeof(float), st));
+    dim3 tgrid((N + 31) / 32, (K + 31) / 32);
+    if (split) {
+        hf::tc::transpose_b<true><<<tgrid, 256, 0, st>>>(B, Bt, K, N);
+        HF_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&A3), static_cast<size_t>(M) * Ke * sizeof(float), st));
+        hf::tc::split3_a<<<hf::num_sms(device) * 8, 256, 0, st>>>(A, A3, M, K);
+    } else {
+        hf::tc::transpose_b<false><<<tgrid, 256, 0, st>>>(B, Bt, K, N);
+    }
     HF_CHECK_LAUNCH();
-    int rc = hf::tc::launch(A3, B3, C, M, N, 3 * K, device, st);
-    cudaFreeAsync(A3, st);
-    cudaFreeAsync(B3, st);
+    int rc = hf::tc::launch(split ? A3 : A, Bt, C, M, N, Ke, device, st);
+    cudaFreeAsync(Bt, st);
+    if (A3) cudaFreeAsync(A3, st);
     return rc;
 }

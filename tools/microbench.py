@@ -30,7 +30,12 @@ def main():
     dev = torch.device("cuda:0")
     for n in (1 << 20, 1 << 24, 1 << 28):
         for Kr in (2, 3, 5):
-            reps = [torch.rand(n, device=dev) + 1 for _ in range(Kr)]
+            # realistic replicas: diverse variants differ by ~1e-6 relative,
+            # plus one injected bit flip
+            base = torch.rand(n, device=dev) + 1
+            reps = [base * (1 + 1e-6 * torch.randn(n, device=dev)) for _ in range(Kr)]
+            kernels.inject_bitflip(reps[-1], n // 3, 25)
+            del base
             voted = torch.empty_like(reps[0])
             ws = kernels.VoteWorkspace(0)
             t = timeit(lambda: kernels.vote_async(reps, ws, 1e-3, voted=voted))
