@@ -6,27 +6,42 @@
 // tensor cores, accumulates every output in fp32 in ascending k order with
 // fused multiply-add, and so fails independently of the tcgen05 variant.
 //
-// Fast path (M%128 == N%128 == 0, K%8 == 0, 16B-aligned): 128x128x8 CTA
-// tile, 256 threads, 8x8 outputs per thread as 2x2 blocks of 4x4, A staged
-// transposed in shared memory, two smem stages with a register prefetch of the
-// next k-tile, one barrier per k-tile, register double-buffered fragments.  Warps are laid out 4x2 over the
+// Fast path (M%128 == N%128 == 0, K%32 == 0, 16B-aligned): A is transposed
+// once by a tiled pre-pass (~2|A| bytes, ~1% of the GEMM) so both operands
+// stream as contiguous k-rows; 128x128x16 CTA tile, 256 threads, 8x8 outputs
+// per thread as 2x2 blocks of 4x4, cp.async 3-stage smem ring, one barrier
+// per k-tile, register double-buffered fragments, two CTAs per SM.  Warps are laid out 4x2 over the
 // 16x16 thread grid so each LDS.128 of A and of B is one wavefront.
 // Generic path: 16x16 bounds-checked tiles for ragged shapes.
 #include "common.cuh"
 
 namespace hf {
 
-constexpr int SB_M = 128, SB_N = 128, SB_K = 8, S_PAD = 4;
+constexpr int SB_M = 128, SB_N = 128, SB_K = 16, S_STAGES = 3;
 
-// 128x128x8 CTA tile, 256 threads, 8x8 per thread; fragments for k+1 are
-// loaded from shared memory while k is multiplied (register double buffer),
-// the next k-tile is prefetched from global into registers; <= 128 registers
-// so two CTAs (16 warps) share an SM.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// 128x128x16 CTA tile, 256 threads, 8x8 outputs per thread.  Operands are
+// A^T (K x M, from the transpose pre-pass) and B (K x N): both k-tiles are
+// 16 rows of 512 contiguous bytes, streamed by cp.async into a 3-stage smem
+// ring without staging registers; fragments for k+1 are read from smem
+// while k is multiplied.  <= 128 registers: two CTAs (16 warps) per SM hide
+// each other's barrier and latency stalls.
 __global__ void __launch_bounds__(256, 2)
-sgemm_128x128(const float* __restrict__ A, const float* __restrict__ B, float* __restrict__ C,
+sgemm_128x128(const float* __restrict__ At, const float* __restrict__ B, float* __restrict__ C,
               int M, int N, int K) {
-    __shared__ __align__(16) float As[2][SB_K][SB_M + S_PAD];
-    __shared__ __align__(16) float Bs[2][SB_K][SB_N];
+    extern __shared__ __align__(16) float sm[];
+    float* As = sm;                                   // [S][SB_K][SB_M]
+    float* Bs = sm + S_STAGES * SB_K * SB_M;          // [S][SB_K][SB_N]
 
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;
@@ -46,11 +61,23 @@ sgemm_128x128(const float* __restrict__ A, const float* __restrict__ B, float* _
     const int tn = (bid % per_group) / gm;
     const int m0 = tm * SB_M, n0 = tn * SB_N;
 
-    // global->smem mapping: A 128x8 (one float4 per thread), B 8x128 (one float4)
-    const int a_row = t >> 1, a_k = (t & 1) * 4;
-    const int b_k = t >> 5, b_n = (t & 31) * 4;
-    const float* Ag = A + static_cast<long long>(m0 + a_row) * K + a_k;
-    const float* Bg = B + static_cast<long long>(b_k) * N + n0 + b_n;
+    // copy mapping: each of the 16 k-rows is 32 chunks of 16 B per operand;
+    // thread t moves chunk (t & 31) of rows (t >> 5) and (t >> 5) + 8
+    const int c_row = t >> 5, c_col = (t & 31) * 4;
+    const float* Ag = At + static_cast<long long>(c_row) * M + m0 + c_col;
+    const float* Bg = B + static_cast<long long>(c_row) * N + n0 + c_col;
+    const long long a8 = 8LL * M, b8 = 8LL * N;
+
+    auto issue = [&](int kt, int stage) {
+        const long long ka = static_cast<long long>(kt) * SB_K * M;
+        const long long kb = static_cast<long long>(kt) * SB_K * N;
+        float* as = As + stage * SB_K * SB_M + c_row * SB_M + c_col;
+        float* bs = Bs + stage * SB_K * SB_N + c_row * SB_N + c_col;
+        cp_async16(as, Ag + ka);
+        cp_async16(as + 8 * SB_M, Ag + ka + a8);
+        cp_async16(bs, Bg + kb);
+        cp_async16(bs + 8 * SB_N, Bg + kb + b8);
+    };
 
     float acc[8][8];
 #pragma unroll
@@ -58,49 +85,36 @@ sgemm_128x128(const float* __restrict__ A, const float* __restrict__ B, float* _
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
 
-    float4 ra = __ldg(reinterpret_cast<const float4*>(Ag));
-    float4 rb = __ldg(reinterpret_cast<const float4*>(Bg));
-    As[0][a_k + 0][a_row] = ra.x;
-    As[0][a_k + 1][a_row] = ra.y;
-    As[0][a_k + 2][a_row] = ra.z;
-    As[0][a_k + 3][a_row] = ra.w;
-    *reinterpret_cast<float4*>(&Bs[0][b_k][b_n]) = rb;
-    __syncthreads();
-
-    float4 fa[2][2], fb[2][2];
-    fa[0][0] = *reinterpret_cast<const float4*>(&As[0][0][ty * 4]);
-    fa[0][1] = *reinterpret_cast<const float4*>(&As[0][0][64 + ty * 4]);
-    fb[0][0] = *reinterpret_cast<const float4*>(&Bs[0][0][tx * 4]);
-    fb[0][1] = *reinterpret_cast<const float4*>(&Bs[0][0][64 + tx * 4]);
-
     const int nk = K / SB_K;
+#pragma unroll
+    for (int s = 0; s < S_STAGES - 1; ++s) {
+        if (s < nk) issue(s, s);
+        cp_async_commit();
+    }
+
     for (int kt = 0; kt < nk; ++kt) {
-        const int s = kt & 1;
-        const bool more = kt + 1 < nk;
-        if (more) {
-            ra = __ldg(reinterpret_cast<const float4*>(Ag + (kt + 1) * SB_K));
-            rb = __ldg(reinterpret_cast<const float4*>(Bg + static_cast<long long>((kt + 1) * SB_K) * N));
+        cp_async_wait<S_STAGES - 2>();
+        __syncthreads();
+        {
+            const int nt = kt + S_STAGES - 1;
+            if (nt < nk) issue(nt, nt % S_STAGES);
+            cp_async_commit();
         }
+        const float* as = As + (kt % S_STAGES) * SB_K * SB_M;
+        const float* bs = Bs + (kt % S_STAGES) * SB_K * SB_N;
+        float4 fa[2][2], fb[2][2];
+        fa[0][0] = *reinterpret_cast<const float4*>(as + ty * 4);
+        fa[0][1] = *reinterpret_cast<const float4*>(as + 64 + ty * 4);
+        fb[0][0] = *reinterpret_cast<const float4*>(bs + tx * 4);
+        fb[0][1] = *reinterpret_cast<const float4*>(bs + 64 + tx * 4);
 #pragma unroll
         for (int k = 0; k < SB_K; ++k) {
             const int cur = k & 1, nxt = cur ^ 1;
             if (k + 1 < SB_K) {
-                fa[nxt][0] = *reinterpret_cast<const float4*>(&As[s][k + 1][ty * 4]);
-                fa[nxt][1] = *reinterpret_cast<const float4*>(&As[s][k + 1][64 + ty * 4]);
-                fb[nxt][0] = *reinterpret_cast<const float4*>(&Bs[s][k + 1][tx * 4]);
-                fb[nxt][1] = *reinterpret_cast<const float4*>(&Bs[s][k + 1][64 + tx * 4]);
-            } else if (more) {
-                // stage the prefetched tile, then start the next tile's fragments
-                As[s ^ 1][a_k + 0][a_row] = ra.x;
-                As[s ^ 1][a_k + 1][a_row] = ra.y;
-                As[s ^ 1][a_k + 2][a_row] = ra.z;
-                As[s ^ 1][a_k + 3][a_row] = ra.w;
-                *reinterpret_cast<float4*>(&Bs[s ^ 1][b_k][b_n]) = rb;
-                __syncthreads();
-                fa[nxt][0] = *reinterpret_cast<const float4*>(&As[s ^ 1][0][ty * 4]);
-                fa[nxt][1] = *reinterpret_cast<const float4*>(&As[s ^ 1][0][64 + ty * 4]);
-                fb[nxt][0] = *reinterpret_cast<const float4*>(&Bs[s ^ 1][0][tx * 4]);
-                fb[nxt][1] = *reinterpret_cast<const float4*>(&Bs[s ^ 1][0][64 + tx * 4]);
+                fa[nxt][0] = *reinterpret_cast<const float4*>(as + (k + 1) * SB_M + ty * 4);
+                fa[nxt][1] = *reinterpret_cast<const float4*>(as + (k + 1) * SB_M + 64 + ty * 4);
+                fb[nxt][0] = *reinterpret_cast<const float4*>(bs + (k + 1) * SB_N + tx * 4);
+                fb[nxt][1] = *reinterpret_cast<const float4*>(bs + (k + 1) * SB_N + 64 + tx * 4);
             }
             const float a[8] = {fa[cur][0].x, fa[cur][0].y, fa[cur][0].z, fa[cur][0].w,
                                 fa[cur][1].x, fa[cur][1].y, fa[cur][1].z, fa[cur][1].w};
@@ -112,6 +126,7 @@ sgemm_128x128(const float* __restrict__ A, const float* __restrict__ B, float* _
                 for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
         }
     }
+    cp_async_wait<0>();
 
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -121,6 +136,20 @@ sgemm_128x128(const float* __restrict__ A, const float* __restrict__ B, float* _
         *reinterpret_cast<float4*>(crow + 64 + tx * 4) =
             make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
     }
+}
+
+constexpr int SGEMM_SMEM = S_STAGES * SB_K * (SB_M + SB_N) * 4;
+
+// A (M x K) -> At (K x M), 32x32 tiles through padded smem.
+__global__ void __launch_bounds__(256) transpose_a(const float* __restrict__ A, float* __restrict__ At, int M, int K) {
+    __shared__ float tile[32][33];
+    const int m0 = blockIdx.y * 32, k0 = blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+    for (int r = ty; r < 32; r += 8) tile[r][tx] = A[static_cast<long long>(m0 + r) * K + k0 + tx];
+    __syncthreads();
+#pragma unroll
+    for (int r = ty; r < 32; r += 8) At[static_cast<long long>(k0 + r) * M + m0 + tx] = tile[tx][r];
 }
 
 // Generic bounds-checked path.
@@ -154,9 +183,19 @@ extern "C" int hf_gemm_simt(const float* A, const float* B, float* C, int M, int
     cudaStream_t st = hf::as_stream(stream);
     bool aligned = (reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) |
                     reinterpret_cast<uintptr_t>(C)) % 16 == 0;
-    if (aligned && M % hf::SB_M == 0 && N % hf::SB_N == 0 && K % hf::SB_K == 0) {
+    if (aligned && M % hf::SB_M == 0 && N % hf::SB_N == 0 && K % 32 == 0) {
+        static bool attr[64] = {false};
+        if (!attr[device]) {
+            HF_CUDA_CHECK(cudaFuncSetAttribute(hf::sgemm_128x128, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               hf::SGEMM_SMEM));
+            attr[device] = true;
+        }
+        float* At = nullptr;
+        HF_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&At), static_cast<size_t>(M) * K * sizeof(float), st));
+        hf::transpose_a<<<dim3(K / 32, M / 32), 256, 0, st>>>(A, At, M, K);
         int tiles = (M / hf::SB_M) * (N / hf::SB_N);
-        hf::sgemm_128x128<<<tiles, 256, 0, st>>>(A, B, C, M, N, K);
+        hf::sgemm_128x128<<<tiles, 256, hf::SGEMM_SMEM, st>>>(At, B, C, M, N, K);
+        cudaFreeAsync(At, st);
     } else {
         dim3 grid((N + 15) / 16, (M + 15) / 16);
         hf::sgemm_generic<<<grid, 256, 0, st>>>(A, B, C, M, N, K);

@@ -110,6 +110,14 @@ struct Elem;
 // (each RN32 step is within 2^-24 relative when its result is a finite
 // normal number, which the guard checks; binary64 rounding of |a-b| and δm
 // moves them by 2^-53 only, so neither decision can flip).
+// Rare path, kept out of line so the compiler cannot if-convert it into the
+// common path.
+__device__ __noinline__ bool f32_slow(uint32_t a, uint32_t b, double delta, long long ulp) {
+    bool r = rel_ok(static_cast<double>(__uint_as_float(a)), static_cast<double>(__uint_as_float(b)), delta);
+    if (!r && ulp >= 0) r = ulp_ok32(a, b, ulp);
+    return r;
+}
+
 template <>
 struct Elem<HF_F32> {
     using T = uint32_t;
@@ -120,14 +128,10 @@ struct Elem<HF_F32> {
         const float d = fabsf(fa - fb);
         const float m = fmaxf(fabsf(fa), fabsf(fb));
         const float tl = dl * m, th = dh * m;
-        bool r;
-        if (d < INFINITY && th < INFINITY && tl >= 1.17549435e-38f && !(d > tl && d < th)) {
-            r = d <= tl;
-        } else {
-            r = rel_ok(static_cast<double>(fa), static_cast<double>(fb), delta);
-        }
-        if (!r && ulp >= 0) r = ulp_ok32(a, b, ulp);
-        return r;
+        const bool sure = d < INFINITY && th < INFINITY && tl >= 1.17549435e-38f;
+        if (__builtin_expect(sure && d <= tl, 1)) return true;
+        if (sure && d >= th && ulp < 0) return false;
+        return f32_slow(a, b, delta, ulp);
     }
 };
 
@@ -179,57 +183,85 @@ struct Acc {
     unsigned long long first;
 };
 
+template <typename T, int K>
+struct Vals {
+    T v[K];
+};
+
+// General K-way vote of one element (rare path: replica 0 is not in the
+// majority).  m0 = agreement mask of replica 0, already computed.  Lazy pair
+// evaluation in replica order: when replica r is evaluated all its pairs are
+// known (pairs (r', r) for r' < r were computed earlier), so the first r
+// reaching a majority is v(i).  Returns bits [0,K) = replicas disagreeing with
+// the voted value, bit 8 = unresolved, bits [16,20) = v.
+template <int DT, int K>
+__device__ __noinline__ uint32_t vote_elem_slow(const Vals<typename Elem<DT>::T, K> x, const VoteParams& p,
+                                                uint32_t m0) {
+    using E = Elem<DT>;
+    uint32_t agree[K];
+    agree[0] = m0;
+#pragma unroll
+    for (int r = 1; r < K; ++r) agree[r] = (1u << r) | ((m0 >> r) & 1u);
+    int v = -1;
+#pragma unroll
+    for (int r = 1; r < K; ++r) {
+        if (v >= 0) break;
+#pragma unroll
+        for (int s = r + 1; s < K; ++s) {
+            const int pi = pair_index<K>(r, s);
+            if (E::ok(x.v[r], x.v[s], p.pdelta[pi], p.pdl[pi], p.pdh[pi], p.pulp[pi])) {
+                agree[r] |= 1u << s;
+                agree[s] |= 1u << r;
+            }
+        }
+        if (2 * __popc(agree[r]) > K) v = r;  // 2*(agree_r + 1) > K
+    }
+    constexpr uint32_t full = (1u << K) - 1u;
+    if (v < 0) return full | 0x100u;
+    uint32_t m = 0;
+#pragma unroll
+    for (int r = 1; r < K; ++r)
+        if (v == r) m = agree[r];
+    return (~m & full) | (static_cast<uint32_t>(v) << 16);
+}
+
 // Vote one element given its K raw values; returns the voted raw value.
+// Common path: replica 0's K-1 pair predicates; if replica 0 is in the
+// majority it is v(i) (the lowest majority replica) and every count follows
+// from its agreement mask.
 template <int DT, int K>
 __device__ __forceinline__ typename Elem<DT>::T vote_elem(const typename Elem<DT>::T (&x)[K],
                                                            const VoteParams& p, Acc<K>& acc,
                                                            unsigned long long idx) {
     using E = Elem<DT>;
-    // Lazy pair evaluation in replica order: when replica r is evaluated all
-    // its pairs are known (pairs (r', r) for r' < r were computed earlier), so
-    // the first r reaching a majority is v(i).  When every replica agrees this
-    // costs K-1 pair predicates instead of K(K-1)/2.
-    uint32_t agree[K];
+    uint32_t m0 = 1u;
 #pragma unroll
-    for (int r = 0; r < K; ++r) agree[r] = 1u << r;
-    int v = -1;
-#pragma unroll
-    for (int r = 0; r < K; ++r) {
-        if (v < 0) {
-#pragma unroll
-            for (int s = r + 1; s < K; ++s) {
-                const int pi = pair_index<K>(r, s);
-                if (E::ok(x[r], x[s], p.pdelta[pi], p.pdl[pi], p.pdh[pi], p.pulp[pi])) {
-                    agree[r] |= 1u << s;
-                    agree[s] |= 1u << r;
-                }
-            }
-            // 2*(agree_r + 1) > K with agree_r counted without self
-            if (2 * __popc(agree[r]) > K) v = r;
-        }
+    for (int s = 1; s < K; ++s) {
+        const int pi = pair_index<K>(0, s);
+        if (E::ok(x[0], x[s], p.pdelta[pi], p.pdl[pi], p.pdh[pi], p.pulp[pi])) m0 |= 1u << s;
     }
-    typename E::T out = x[0];
-    bool flag;
-    if (v < 0) {
-#pragma unroll
-        for (int r = 0; r < K; ++r) acc.mism[r] += 1;
-        acc.unres += 1;
-        flag = true;
+    constexpr uint32_t full = (1u << K) - 1u;
+    if (__builtin_expect(m0 == full, 1)) return x[0];
+    uint32_t dis;
+    int v = 0;
+    if (2 * __popc(m0) > K) {
+        dis = ~m0 & full;
     } else {
-        uint32_t m = 0;
+        Vals<typename E::T, K> xv;
 #pragma unroll
-        for (int r = 0; r < K; ++r) {
-            if (v == r) {
-                m = agree[r];
-                out = x[r];
-            }
-        }
-        const uint32_t full = (1u << K) - 1u;
-#pragma unroll
-        for (int r = 0; r < K; ++r) acc.mism[r] += ((m >> r) & 1u) ^ 1u;
-        flag = (m & full) != full;
+        for (int r = 0; r < K; ++r) xv.v[r] = x[r];
+        const uint32_t res = vote_elem_slow<DT, K>(xv, p, m0);
+        dis = res & full;
+        v = static_cast<int>(res >> 16);
+        acc.unres += (res >> 8) & 1u;
     }
-    if (flag && acc.first == ~0ull) acc.first = idx;
+#pragma unroll
+    for (int r = 0; r < K; ++r) acc.mism[r] += (dis >> r) & 1u;
+    if (acc.first == ~0ull) acc.first = idx;
+    typename E::T out = x[0];
+#pragma unroll
+    for (int r = 1; r < K; ++r)
+        if (v == r) out = x[r];
     return out;
 }
 

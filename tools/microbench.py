@@ -72,6 +72,24 @@ def main():
         t = timeit(lambda: torch.matmul(a, b, out=c), iters=5)
         out.append({"k": "cublas_fp32", "N": N, "ms": t * 1e3, "TFLOPs": 2 * N ** 3 / t / 1e12})
         print(json.dumps(out[-1]), flush=True)
+    # accuracy of each variant vs the binary64 oracle (U[1,2) operands)
+    import numpy as np
+    for N in (1024, 2048):
+        rng = np.random.default_rng(N)
+        a = rng.uniform(1, 2, (N, N)).astype(np.float32)
+        b = rng.uniform(1, 2, (N, N)).astype(np.float32)
+        ref = a.astype(np.float64) @ b.astype(np.float64)
+        ta, tb = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+        c = torch.empty(N, N, device=dev)
+        errs = {}
+        for name, fn in (("simt", lambda: kernels.gemm_simt(ta, tb, c)),
+                         ("tc_tf32", lambda: kernels.gemm_tc(ta, tb, c, mode=0)),
+                         ("tc_3xtf32", lambda: kernels.gemm_tc(ta, tb, c, mode=1))):
+            fn()
+            torch.cuda.synchronize()
+            errs[name] = float(np.max(np.abs(c.cpu().numpy() - ref) / np.abs(ref)))
+        out.append({"k": "accuracy", "N": N, "max_rel_err": errs})
+        print(json.dumps(out[-1]), flush=True)
     Path("gpurun_out").mkdir(exist_ok=True)
     Path("gpurun_out/microbench.json").write_text(json.dumps(out, indent=1))
 
