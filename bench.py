@@ -1,0 +1,478 @@
+"""Benchmark of the voted-task hot path (driver contract: one JSON line).
+
+Workload (BASELINE.json configs[1], "C2"): dual-modular redundancy of a
+4096x4096 fp32 matmul task on one B200 — the tcgen05 TF32 variant (unit
+gpu0.tc) and the SIMT FP32 variant (unit gpu0.simt) run as replicas through
+the drop-in Runtime (DMR strategy), protected attempts checkpoint their
+device-resident inputs (hf_checkpoint into a reserve HBM space), seeded
+bit-flip faults are injected at a fixed per-replica probability, hf_vote
+decides, mismatches are re-run.  A "step" is one voted task.
+
+  value  tasks/s with A, B already resident in HBM (sole device copies)
+  e2e    tasks/s through the same public API with HOST buffers: per step the
+         pinned inputs are copied host->device inside invoke() and the
+         committed C is read back device->host (read_into)
+N > 1: one process per GPU, each running its own independent task stream
+(weak scaling, no data-path collective); timing is max over ranks.
+
+--impl reference times the reference's own CPU implementation of the same
+task (hetrt from baseline/_ref through its public Runtime API, numpy bodies,
+its voting.compare) on the host cores; without baseline/_ref the oracle port
+(oracle/: numpy matmul + restated voter) is timed instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("hetft", "reference"), default="hetft")
+    ap.add_argument("--n", type=int, default=4096)
+    ap.add_argument("--fault-prob", type=float, default=0.05, help="per-replica corrupt (bit flip) probability")
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-s", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---- clocks sampling -----------------------------------------------------------------
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+        self._t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.QUERY}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self._t = threading.Thread(target=self._read, daemon=True)
+        self._t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self._t is not None:
+            self._t.join(timeout=2)
+        sm, smax, power, reasons = [], None, [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+                power.append(float(f[3]))
+            except ValueError:
+                continue
+            for name, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "power_w_max": max(power) if power else None, "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ---- reference / CPU arm ------------------------------------------------------------------
+
+def _reference_module():
+    ref = ROOT / "baseline" / "_ref"
+    if (ref / "hetrt").exists():
+        sys.path.insert(0, str(ref))
+        import hetrt  # noqa: F401
+        return hetrt
+    return None
+
+
+def reference_tasks(n: int, count_or_seconds, seed: int, by_time: bool):
+    """Run DMR n x n matmul tasks with the reference CPU implementation.
+    Returns (tasks, seconds, kind, detail)."""
+    hetrt = _reference_module()
+    rng = np.random.default_rng(seed)
+    a = rng.uniform(1, 2, (n, n)).astype(np.float32)
+    b = rng.uniform(1, 2, (n, n)).astype(np.float32)
+    if hetrt is not None:
+        cfg = {"memory_spaces": [{"id": "host", "host": True}],
+               "units": [{"id": "cpu0", "kind": "cpu", "memory_space": "host", "seed": 1},
+                         {"id": "cpu1", "kind": "cpu", "memory_space": "host", "seed": 2}]}
+        rt = hetrt.Runtime(hetrt.load_fleet(cfg), hetrt.RuntimeConfig(serial_replicas=True))
+        task = rt.declare_task("matmul", (hetrt.Param.area("A", "r"), hetrt.Param.area("B", "r"),
+                                          hetrt.Param.area("C", "w"), hetrt.Param.scalar("n")))
+
+        def body(ctx):
+            k = ctx.arg("n")
+            A = ctx.request("A", "r").reshape(k, k)
+            B = ctx.request("B", "r").reshape(k, k)
+            C = ctx.request("C", "w").reshape(k, k)
+            np.matmul(A, B, out=C)
+
+        rt.attach_kernel(task, "mm_cpu", "cpu", body)
+        zeros = bytes(4 * n * n)
+
+        def one():
+            ia = rt.register_data(a.tobytes(), n * n, hetrt.ValueType.FLOAT32, "r")
+            ib = rt.register_data(b.tobytes(), n * n, hetrt.ValueType.FLOAT32, "r")
+            ic = rt.register_data(zeros, n * n, hetrt.ValueType.FLOAT32, "w")
+            rep = rt.invoke(task, {"A": ia, "B": ib, "C": ic, "n": n}, hetrt.Strategy(hetrt.StrategyKind.DMR))
+            rt.read_area(ic)
+            assert rep.success
+        kind, detail = "reference", "hetrt (baseline/_ref) Runtime.invoke DMR: 2 numpy matmul bodies + voting.compare"
+    else:
+        from oracle import vote as ovote
+
+        def one():
+            c0 = a @ b
+            c1 = a @ b
+            ovote.vote([c0, c1], 1e-3)
+        kind, detail = "port", "oracle port: 2 numpy matmuls + oracle.vote (reference absent)"
+    t0 = time.perf_counter()
+    done = 0
+    while True:
+        one()
+        done += 1
+        el = time.perf_counter() - t0
+        if by_time and el >= count_or_seconds and done >= 1:
+            break
+        if not by_time and done >= count_or_seconds:
+            break
+    return done, time.perf_counter() - t0, kind, detail
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    n = args.n
+    reference_tasks(n, max(1, args.warmup // 3), args.seed, by_time=False)   # warm caches/BLAS
+    tasks, secs, kind, detail = reference_tasks(n, args.steps, args.seed, by_time=False)
+    v = tasks / secs
+    line = {"metric": "voted tasks/sec (DMR 4096^2 fp32 matmul, TC vs SIMT variants)", "value": v,
+            "unit": "tasks/s", "n_gpus": args.gpus, "steps": tasks, "warmup": args.warmup,
+            "ms_per_step": 1e3 * secs / tasks, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic U[1,2) fp32 operands",
+            "config": {"workload": f"C2: DMR {n}x{n} fp32 matmul, detect-and-rerun", "n": n},
+            "impl": "reference",
+            "cpu_baseline": {"value": v, "unit": "tasks/s", "cores": host_cores(), "kind": kind,
+                             "sample": f"{tasks} tasks: {detail}"},
+            "e2e": {"value": v, "unit": "tasks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---- B200 arm ---------------------------------------------------------------------------------
+
+def build_runtime(device: int, fault_prob: float, seed: int):
+    import paper_1405_2912_b200 as hf
+    cfg = hf.gpu_fleet_config(devices=(device,), kinds=("gpu-tc", "gpu-simt"))
+    cfg["memory_spaces"].append({"id": f"gpu{device}ckpt", "device": device, "label": "HBM checkpoint reserve"})
+    for i, u in enumerate(cfg["units"]):
+        u.update({"corrupt_prob": fault_prob, "corrupt_mode": "bitflip", "seed": seed * 1_000_003 + i * 101 + 17})
+    fleet = hf.load_fleet(cfg)
+    rt = hf.Runtime(fleet, hf.RuntimeConfig(checkpoint_space=f"gpu{device}ckpt", serial_replicas=True,
+                                            attempt_limit=64))
+    task = hf.get_workload("matmul").attach(rt, kinds=("gpu-tc", "gpu-simt"))
+    return hf, rt, task
+
+
+def run_hetft_arm(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+
+    device = local if torch.cuda.device_count() > local else 0
+    torch.cuda.set_device(device)
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{device}"))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{device}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    hf, rt, task = build_runtime(device, args.fault_prob, args.seed + 7919 * rank)
+    from paper_1405_2912_b200 import kernels
+    n = args.n
+    nb = n * n * 4
+    space = f"gpu{device}mem"
+    gen = torch.Generator(device=f"cuda:{device}")
+    gen.manual_seed(args.seed * 7919 + rank)
+    A = (torch.rand(n * n, device=f"cuda:{device}", generator=gen) + 1).view(torch.uint8)
+    B = (torch.rand(n * n, device=f"cuda:{device}", generator=gen) + 1).view(torch.uint8)
+    C0 = torch.zeros(nb, dtype=torch.uint8, device=f"cuda:{device}")
+    strat = hf.Strategy(hf.StrategyKind.HET_DMR)
+    stream = rt.backend.stream(device)
+
+    stats = {"tasks": 0, "rounds": 0, "votes": {}, "injected": 0, "mismatch": 0, "vote_ns": 0,
+             "attempt_ns": {}, "attempt_n": {}}
+
+    def device_step(record: bool):
+        ia = rt.register_device_data(A, n * n, hf.ValueType.FLOAT32, "r", space)
+        ib = rt.register_device_data(B, n * n, hf.ValueType.FLOAT32, "r", space)
+        ic = rt.register_device_data(C0, n * n, hf.ValueType.FLOAT32, "w", space)
+        rep = rt.invoke(task, {"A": ia, "B": ib, "C": ic, "n": n}, strat)
+        if not rep.success:
+            raise RuntimeError("task failed")
+        if record:
+            stats["tasks"] += 1
+            stats["rounds"] += rep.rounds
+            for v in rep.votes:
+                stats["votes"][v] = stats["votes"].get(v, 0) + 1
+            stats["injected"] += len(rep.injected)
+            stats["mismatch"] += rep.fault_counts["vote_mismatch"]
+            stats["vote_ns"] += rep.voter_ns
+        for a in (ia, ib, ic):
+            rt.release(a)
+        return rep
+
+    # trace per-kernel durations via the executor's measured attempts
+    def on_trace(line: str):
+        if line.startswith("ATT") and "fault=none" in line:
+            f = dict(kv.split("=", 1) for kv in line.split()[1:] if "=" in kv)
+            k = f["kernel"]
+            stats["attempt_ns"][k] = stats["attempt_ns"].get(k, 0) + int(f["duration_ns"])
+            stats["attempt_n"][k] = stats["attempt_n"].get(k, 0) + 1
+
+    for _ in range(args.warmup):
+        device_step(False)
+    torch.cuda.synchronize()
+
+    # ---- timed region: device-resident inputs ----
+    rt.executor._trace = on_trace
+    sampler = ClockSampler(device) if rank == 0 else None
+    barrier()
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.start()
+    launches0 = kernels.LAUNCHES
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        device_step(True)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop() if sampler else None
+    launches = kernels.LAUNCHES - launches0
+    rt.executor._trace = None
+    t_dev = ev0.elapsed_time(ev1) * 1e-3
+    t_max = max_over_ranks(t_dev)
+
+    # ---- e2e: host buffers through the same API (H2D inside invoke, D2H read) ----
+    e2e_steps = args.e2e_steps or max(3, args.steps // 2)
+    hA = torch.empty(nb, dtype=torch.uint8).pin_memory()
+    hB = torch.empty(nb, dtype=torch.uint8).pin_memory()
+    hC = torch.empty(nb, dtype=torch.uint8).pin_memory()
+    hZ = torch.zeros(nb, dtype=torch.uint8).pin_memory()
+    hA.copy_(A.cpu())
+    hB.copy_(B.cpu())
+
+    def host_step():
+        ia = rt.register_host_buffer(hA, n * n, hf.ValueType.FLOAT32, "r")
+        ib = rt.register_host_buffer(hB, n * n, hf.ValueType.FLOAT32, "r")
+        ic = rt.register_host_buffer(hZ, n * n, hf.ValueType.FLOAT32, "w")
+        rep = rt.invoke(task, {"A": ia, "B": ib, "C": ic, "n": n}, strat)
+        rt.read_into(ic, hC)
+        for a in (ia, ib, ic):
+            rt.release(a)
+        return rep
+
+    host_step()
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        host_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    t_e2e = max_over_ranks(e0.elapsed_time(e1) * 1e-3)
+
+    # ---- kernel-level measurements (same process, after the timed regions) ----
+    kern = kernel_rooflines(device, n, kernels, torch)
+
+    total_tasks = args.steps * world
+    if rank != 0:
+        return
+    peaks, peak_src = load_peaks()
+    simt_ns = stats["attempt_ns"].get("mm_simt", 0) / max(1, stats["attempt_n"].get("mm_simt", 1))
+    tc_ns = stats["attempt_ns"].get("mm_tc", 0) / max(1, stats["attempt_n"].get("mm_tc", 1))
+    flops = 2.0 * n ** 3
+    simt_tflops = flops / (simt_ns * 1e-9) / 1e12 if simt_ns else None
+    sm_max = (clocks or {}).get("sm_max_mhz") or 1965.0
+    ffma_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12
+    vote_gbs = (stats["votes"] and stats["vote_ns"]) and \
+        (2 * nb * sum(stats["votes"].values())) / (stats["vote_ns"] * 1e-9) / 1e9
+    cpu = None
+    if not args.no_cpu_baseline:
+        tasks, secs, kind, detail = reference_tasks(n, args.cpu_sample_s, args.seed, by_time=True)
+        cpu = {"value": tasks / secs, "unit": "tasks/s", "cores": host_cores(), "kind": kind,
+               "sample": f"{tasks} tasks in {secs:.1f} s: {detail}"}
+    line = {
+        "metric": "voted tasks/sec (DMR 4096^2 fp32 matmul, TC vs SIMT variants)",
+        "value": total_tasks / t_max,
+        "unit": "tasks/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1e3 * t_max / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic U[1,2) fp32 operands generated on device (no dataset)",
+        "config": {"workload": f"C2: DMR {n}x{n} fp32 matmul, tcgen05-TF32 vs SIMT-FP32 replicas, "
+                               f"HBM checkpoint of inputs, bit-flip faults p={args.fault_prob}/replica, "
+                               f"hf_vote detect-and-rerun", "n": n, "replicas": 2,
+                   "strategy": "hetdmr", "parallelism": f"independent task streams x{world}",
+                   "l2": "operands (3 x 64 MiB) exceed the 126 MB L2; no flush needed"},
+        "e2e": {"value": (e2e_steps * world) / t_e2e, "unit": "tasks/s", "h2d_bytes_per_step": 2 * nb,
+                "d2h_bytes_per_step": nb},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "roofline": {"bound": "fp32-simt", "kernel": "hf_gemm_simt (incl. A^T pre-pass)",
+                     "achieved": simt_tflops, "peak": ffma_peak, "unit": "TFLOP/s",
+                     "frac": (simt_tflops / ffma_peak) if simt_tflops else None, "traffic": None,
+                     "peak_source": f"nominal FFMA 148 SM x 128 lanes x 2 flop x {sm_max:.0f} MHz "
+                                    "(MEASURED_PEAKS.json has no FP32 SIMT figure)",
+                     "algorithmic": f"2*{n}^3 flop per launch"},
+        "rooflines": kern,
+        "replica_ms": {"mm_simt": simt_ns * 1e-6, "mm_tc": tc_ns * 1e-6},
+        "voter_gbs_in_task": vote_gbs,
+        "faults": {"injected": stats["injected"], "detected_mismatch_votes": stats["mismatch"],
+                   "votes": stats["votes"], "rounds": stats["rounds"]},
+        "cpu_baseline": cpu,
+        "peaks": {"source": peak_src, **peaks},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"]}, "MEASURED_PEAKS.json"
+    return dict(PEAKS_FALLBACK), "fallback (B200_PROFILING.md)"
+
+
+def kernel_rooflines(device, n, kernels, torch):
+    """Per-kernel rooflines: vote / checkpoint vs HBM, TC GEMM vs tensor, all
+    CUDA-event timed on the launching stream over operands > L2."""
+    peaks, _ = load_peaks()
+    st = torch.cuda.Stream(device=device)
+    d = f"cuda:{device}"
+    out = {}
+
+    def time_it(fn, iters=10):
+        with torch.cuda.stream(st):
+            for _ in range(3):
+                fn()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(iters):
+                fn()
+            e1.record(st)
+        st.synchronize()
+        return e0.elapsed_time(e1) * 1e-3 / iters
+
+    m = n * n
+    base = torch.rand(m, device=d) + 1
+    reps = [base * (1 + 1e-6 * torch.randn(m, device=d)) for _ in range(3)]
+    kernels.inject_bitflip(reps[2], m // 3, 27, stream=st)
+    ws = kernels.VoteWorkspace(device, stream=st)
+    for K in (2, 3):
+        t = time_it(lambda: kernels.vote_async(reps[:K], ws, 1e-3, voted=reps[0] if K >= 3 else None, stream=st))
+        byts = K * m * 4      # replica reads; the in-place voted output stores only differing vectors
+        out[f"hf_vote_K{K}"] = {"bound": "hbm", "achieved": byts / t / 1e9, "peak": peaks["hbm_gbs"],
+                                "unit": "GB/s", "frac": byts / t / 1e9 / peaks["hbm_gbs"],
+                                "us": t * 1e6, "algorithmic_bytes": byts,
+                                "note": "voted output written in place over replica 0 (only differing "
+                                        "vectors stored)" if K >= 3 else "no voted output (K = 2 verdict only)"}
+    dst = torch.empty_like(base)
+    t = time_it(lambda: kernels.checkpoint(dst, base, stream=st))
+    out["hf_checkpoint"] = {"bound": "hbm", "achieved": 2 * m * 4 / t / 1e9, "peak": peaks["hbm_gbs"],
+                            "unit": "GB/s", "frac": 2 * m * 4 / t / 1e9 / peaks["hbm_gbs"], "us": t * 1e6,
+                            "algorithmic_bytes": 2 * m * 4}
+    a = base.view(n, n)
+    b = reps[1].view(n, n)
+    c = torch.empty(n, n, device=d)
+    t = time_it(lambda: kernels.gemm_tc(a, b, c, stream=st), iters=10)
+    tf32_peak = peaks["bf16_tflops"] / 2
+    out["hf_gemm_tc"] = {"bound": "tensor", "achieved": 2 * n ** 3 / t / 1e12, "peak": tf32_peak,
+                         "unit": "TFLOP/s", "frac": 2 * n ** 3 / t / 1e12 / tf32_peak, "us": t * 1e6,
+                         "peak_source": "measured bf16 dense / 2 (tf32 rate)", "includes": "B^T + RN pre-pass"}
+    t = time_it(lambda: kernels.gemm_simt(a, b, c, stream=st), iters=5)
+    out["hf_gemm_simt"] = {"bound": "fp32-simt", "achieved": 2 * n ** 3 / t / 1e12, "unit": "TFLOP/s",
+                           "us": t * 1e6}
+    return out
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+    run_hetft_arm(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -127,6 +127,11 @@ int hf_vote_bytes(const void* const* replicas, int K, int64_t n, int elem_width,
 int hf_copy(void* dst, int dst_dev, const void* src, int src_dev,
             int64_t nbytes, void* stream);
 
+/* Fill nbytes of dst (device `device`, or pinned host when device < 0)
+ * with byte `value` (provisional write buffers start zeroed, as the
+ * reference's bytearray(n) does, memory.py:168). Asynchronous. */
+int hf_fill(void* dst, int value, int64_t nbytes, int device, void* stream);
+
 /* Snapshot `buf` into `ckpt` (same device or a peer pointer). If checksum is
  * non-NULL the copy is fused with the position-sensitive 64-bit checksum of
  * the bytes (see hf_checksum) and the call synchronises to return it. */

@@ -39,7 +39,7 @@ HF_GEMM_3XTF32 = 1
 EXPORTED = (
     "hf_init", "hf_last_error", "hf_version", "hf_device_count", "hf_peer_enabled",
     "hf_vote", "hf_vote_workspace_bytes", "hf_vote_workspace_init", "hf_vote_async",
-    "hf_vote_bytes", "hf_copy", "hf_checkpoint", "hf_restore", "hf_checksum",
+    "hf_vote_bytes", "hf_copy", "hf_fill", "hf_checkpoint", "hf_restore", "hf_checksum",
     "hf_inject_bitflip", "hf_inject_scale", "hf_scribble", "hf_gemm_tc", "hf_gemm_simt",
 )
 
@@ -96,6 +96,7 @@ def _declare(lib):
         "hf_vote_bytes": (_i32, [P(_c_void_p), _i32, _i64, _i32, _c_void_p, P(HfVoteResult), _i32,
                                  _c_void_p]),
         "hf_copy": (_i32, [_c_void_p, _i32, _c_void_p, _i32, _i64, _c_void_p]),
+        "hf_fill": (_i32, [_c_void_p, _i32, _i64, _i32, _c_void_p]),
         "hf_checkpoint": (_i32, [_c_void_p, _c_void_p, _i64, P(ctypes.c_uint64), _i32, _c_void_p]),
         "hf_restore": (_i32, [_c_void_p, _c_void_p, _i64, P(ctypes.c_uint64), _i32, _c_void_p]),
         "hf_checksum": (_i32, [_c_void_p, _i64, P(ctypes.c_uint64), _i32, _c_void_p]),

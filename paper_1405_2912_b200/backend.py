@@ -1,0 +1,217 @@
+"""Device backend of the runtime: buffers, streams, timing and the libhetft
+kernels behind the memory manager, fault injection and the voter.
+
+``CudaBackend`` is the only backend the package ships.  Buffers are flat
+uint8 torch tensors: pinned host memory for the host space (device-visible
+through UVA, so the GPU voter can read host replicas zero-copy) and device
+memory for a space bound to a CUDA ordinal.  All data movement and compute
+go through the C-ABI (``kernels`` -> ``_lib`` -> libhetft.so); torch only
+allocates.  There is no CPU fallback: constructing a CudaBackend without a
+CUDA device or without the built library raises.
+
+The backend interface is duck-typed so the reference-mirrored control-plane
+tests can run on a CPU-only machine with a test double (tests/host_backend.py);
+nothing under the package imports or falls back to it.
+"""
+
+from __future__ import annotations
+
+import threading
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib, kernels
+from .devices import INT_DTYPES, MemorySpace, ValueType, view_dtype
+
+_NP_TO_TORCH = {
+    np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64,
+    np.dtype(np.uint8): torch.uint8, np.dtype(np.uint16): torch.uint16,
+    np.dtype(np.uint32): torch.uint32, np.dtype(np.uint64): torch.uint64,
+}
+
+
+def torch_dtype(np_dtype) -> torch.dtype:
+    return _NP_TO_TORCH[np.dtype(np_dtype)]
+
+
+class CudaBackend:
+    """libhetft-backed buffers, copies, injection, voting and timing."""
+
+    name = "cuda"
+
+    def __init__(self):
+        if not torch.cuda.is_available():
+            raise RuntimeError("CudaBackend needs a CUDA device (no CPU fallback exists)")
+        _lib.init()
+        self._streams: dict = {}
+        self._lock = threading.Lock()
+        self.launches = 0             # libhetft kernel launches issued through this backend
+
+    # -- streams / timing ---------------------------------------------------------
+
+    def stream(self, device: Optional[int]):
+        if device is None:
+            return None
+        with self._lock:
+            s = self._streams.get(device)
+            if s is None:
+                s = torch.cuda.Stream(device=device)
+                self._streams[device] = s
+        return s
+
+    def synchronize(self, stream) -> None:
+        if stream is not None:
+            stream.synchronize()
+
+    def timer_start(self, stream, device):
+        if stream is None:
+            import time
+            return ("host", time.perf_counter_ns())
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream)
+        return ("cuda", ev)
+
+    def timer_stop(self, start, stream, device):
+        kind, t0 = start
+        if kind == "host":
+            import time
+            dt = time.perf_counter_ns() - t0
+            return lambda: dt
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream)
+        return lambda: int(t0.elapsed_time(ev) * 1e6)
+
+    def is_device_error(self, exc: BaseException) -> bool:
+        if isinstance(exc, _lib.HfError):
+            return exc.code == _lib.HF_ECUDA
+        return isinstance(exc, torch.cuda.OutOfMemoryError) or "CUDA error" in str(exc)
+
+    # -- buffers ------------------------------------------------------------------
+
+    def alloc(self, space: MemorySpace, nbytes: int, zero: bool = True):
+        if space.device is None:
+            buf = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+            if zero:
+                buf.numpy()[:] = 0
+            return buf
+        with torch.cuda.stream(self.stream(space.device)):
+            buf = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{space.device}")
+        if zero and nbytes:
+            kernels.fill(buf, 0, stream=self.stream(space.device))
+        return buf
+
+    def from_bytes(self, space: MemorySpace, data) -> torch.Tensor:
+        raw = np.frombuffer(bytes(data), dtype=np.uint8)
+        buf = self.alloc(space, raw.size, zero=False)
+        if space.device is None:
+            buf.numpy()[:] = raw
+        else:
+            host = torch.from_numpy(raw.copy()).pin_memory()
+            kernels.copy(buf, host, stream=self.stream(space.device))
+            self.synchronize(self.stream(space.device))
+        return buf
+
+    def to_bytes(self, buf) -> bytes:
+        if buf.device.type == "cuda":
+            self.synchronize(self.stream(buf.device.index))
+            return buf.cpu().numpy().tobytes()
+        return buf.numpy().tobytes()
+
+    def nbytes(self, buf) -> int:
+        return int(buf.numel())
+
+    def element_bytes(self, buf, idx: int, width: int) -> bytes:
+        part = buf[idx * width:(idx + 1) * width]
+        if part.device.type == "cuda":
+            self.synchronize(self.stream(part.device.index))
+            return part.cpu().numpy().tobytes()
+        return part.numpy().tobytes()
+
+    def copy(self, dst, dst_space: MemorySpace, src, src_space: MemorySpace) -> None:
+        """dst <- src on the destination's stream (or the source's when the
+        destination is host memory).  Host<->device copies are ordered after
+        pending work on both sides."""
+        dev = dst_space.device if dst_space.device is not None else src_space.device
+        st = self.stream(dev)
+        if src_space.device is not None and src_space.device != dev:
+            st.wait_stream(self.stream(src_space.device))
+        if dev is None:
+            dst.numpy()[:] = src.numpy()
+            return
+        kernels.copy(dst, src, stream=st)
+        self.launches += 1
+        if dst_space.device is None:
+            self.synchronize(st)   # host readers see the bytes on return
+
+    def checkpoint(self, dst, dst_space: MemorySpace, src, src_space: MemorySpace) -> None:
+        """Snapshot a sole device copy: same-GPU or peer-GPU snapshots use the
+        fused hf_checkpoint stream; host snapshots the copy engine."""
+        if src_space.device is not None and dst_space.device is not None:
+            st = self.stream(src_space.device)
+            kernels.checkpoint(dst, src, stream=st)
+            self.launches += 1
+            return
+        self.copy(dst, dst_space, src, src_space)
+
+    def typed_view(self, buf, value_type: ValueType, width: int, writable: bool):
+        """Element view handed to kernel bodies: numpy for host buffers (the
+        reference's body protocol), a CUDA tensor for device buffers."""
+        dt = view_dtype(value_type, width) if (value_type.numpy_dtype is not None or width in INT_DTYPES) \
+            else np.uint8
+        if buf.device.type == "cuda":
+            return buf.view(torch_dtype(dt))
+        arr = buf.numpy().view(dt)
+        if not writable:
+            arr = arr.view()
+            arr.flags.writeable = False
+        return arr
+
+    # -- fault injection ------------------------------------------------------------
+
+    def _inj_stream(self, buf, stream):
+        dev = buf.device.index if buf.device.type == "cuda" else 0
+        return stream if stream is not None else self.stream(dev)
+
+    # Host-space (CPU unit) outputs live in pinned memory; the injection
+    # kernels reach them through UVA, so every fault is applied on the GPU.
+    def scribble(self, buf, data: bytes, stream=None) -> None:
+        kernels.scribble(buf, data, stream=self._inj_stream(buf, stream))
+        self.launches += 1
+
+    def inject_scale(self, buf, np_dtype, idx: int, rel: float, stream=None) -> None:
+        kernels.inject_scale(buf.view(torch_dtype(np_dtype)), idx, rel, stream=self._inj_stream(buf, stream))
+        self.launches += 1
+
+    def inject_bitflip(self, buf, np_dtype, idx: int, bit: int, stream=None) -> None:
+        kernels.inject_bitflip(buf.view(torch_dtype(np_dtype)), idx, bit, stream=self._inj_stream(buf, stream))
+        self.launches += 1
+
+    # -- voting -----------------------------------------------------------------------
+
+    def vote(self, bufs: Sequence, value_type: ValueType, width: int, rel_tol, ulp_tol=None,
+             voted=None, device: Optional[int] = None):
+        """K-way vote on the GPU (hf_vote).  Replicas may sit on several GPUs
+        (peer loads over NVLink) or in pinned host memory (UVA loads)."""
+        if device is None:
+            devs = [b.device.index for b in bufs if b.device.type == "cuda"]
+            device = devs[0] if devs else 0
+        st = self.stream(device)
+        for b in bufs:
+            if b.device.type == "cuda" and b.device.index != device:
+                st.wait_stream(self.stream(b.device.index))
+        for b in bufs:
+            if b.device.type == "cuda":
+                st.wait_stream(self.stream(b.device.index))
+        start = self.timer_start(st, device)
+        if value_type.numpy_dtype is None and width not in INT_DTYPES:
+            res = kernels.vote_bytes(list(bufs), width, voted=voted, device=device, stream=st)
+        else:
+            dt = torch_dtype(view_dtype(value_type, width))
+            views = [b.view(dt) for b in bufs]
+            res = kernels.vote(views, rel_tol, ulp_tol, voted=voted.view(dt) if voted is not None else None,
+                               device=device, stream=st)
+        stop = self.timer_stop(start, st, device)
+        self.launches += 1
+        return res, stop()

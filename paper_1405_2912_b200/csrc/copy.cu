@@ -207,6 +207,15 @@ int hf_copy(void* dst, int dst_dev, const void* src, int src_dev, int64_t nbytes
     return HF_OK;
 }
 
+int hf_fill(void* dst, int value, int64_t nbytes, int device, void* stream) {
+    HF_REQUIRE(nbytes >= 0, "hf_fill: negative size");
+    if (nbytes == 0) return HF_OK;
+    HF_REQUIRE(dst != nullptr, "hf_fill: NULL pointer");
+    hf::DeviceGuard g(device >= 0 ? device : -1);
+    HF_CUDA_CHECK(cudaMemsetAsync(dst, value & 0xFF, static_cast<size_t>(nbytes), hf::as_stream(stream)));
+    return HF_OK;
+}
+
 int hf_checkpoint(void* ckpt, const void* buf, int64_t nbytes, uint64_t* checksum, int device,
                   void* stream) {
     HF_REQUIRE(nbytes >= 0, "hf_checkpoint: negative size");

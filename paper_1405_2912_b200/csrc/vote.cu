@@ -49,6 +49,7 @@ struct VoteParams {
     long long pulp[kMaxPairs];  // max(u_r, u_s) per pair, < 0 = ULP rule off
     hf_vote_result* out;
     VoteWorkspace* ws;
+    int in_place;   // voted aliases replica 0: store only vectors whose voted value differs
 };
 
 template <int K>
@@ -293,14 +294,16 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
         for (int u = 0; u < UNROLL; ++u) {
             const long long vj = j + u * gstride;
             T o[PV];
+            bool changed = false;
 #pragma unroll
             for (int e = 0; e < PV; ++e) {
                 T x[K];
 #pragma unroll
                 for (int r = 0; r < K; ++r) x[r] = extract<T, PV>(v[u][r], e);
                 o[e] = vote_elem<DT, K>(x, p, acc, static_cast<unsigned long long>(vj) * PV + e);
+                changed |= o[e] != x[0];
             }
-            if (p.voted != nullptr) {
+            if (p.voted != nullptr && (!p.in_place || changed)) {
                 uint4 w;
                 if constexpr (sizeof(T) == 4) {
                     w = make_uint4(o[0], o[1], o[2], o[3]);
@@ -332,14 +335,16 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
 #pragma unroll
         for (int r = 0; r < K; ++r) v[r] = ld_stream(reinterpret_cast<const uint4*>(p.rep[r]) + j);
         T o[PV];
+        bool changed = false;
 #pragma unroll
         for (int e = 0; e < PV; ++e) {
             T x[K];
 #pragma unroll
             for (int r = 0; r < K; ++r) x[r] = extract<T, PV>(v[r], e);
             o[e] = vote_elem<DT, K>(x, p, acc, static_cast<unsigned long long>(j) * PV + e);
+            changed |= o[e] != x[0];
         }
-        if (p.voted != nullptr) {
+        if (p.voted != nullptr && (!p.in_place || changed)) {
             T* dst = reinterpret_cast<T*>(p.voted) + j * PV;
 #pragma unroll
             for (int e = 0; e < PV; ++e) dst[e] = o[e];
@@ -351,7 +356,7 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
 #pragma unroll
         for (int r = 0; r < K; ++r) x[r] = __ldg(reinterpret_cast<const T*>(p.rep[r]) + i);
         T o = vote_elem<DT, K>(x, p, acc, static_cast<unsigned long long>(i));
-        if (p.voted != nullptr) reinterpret_cast<T*>(p.voted)[i] = o;
+        if (p.voted != nullptr && (!p.in_place || o != x[0])) reinterpret_cast<T*>(p.voted)[i] = o;
     }
 
     // ---- reduction: warp -> block (smem) -> one atomic per block ----------
@@ -591,6 +596,7 @@ static int fill_params(VoteParams& p, const void* const* replicas, int K, int64_
         aligned &= reinterpret_cast<uintptr_t>(replicas[r]) % 16 == 0;
     }
     p.voted = static_cast<uint8_t*>(voted);
+    p.in_place = voted != nullptr && voted == replicas[0];
     p.n = n;
     const int per_vec = width <= 8 ? 16 / width : 0;
     p.nvec = (aligned && per_vec > 0) ? n / per_vec : 0;

@@ -17,6 +17,15 @@ import torch
 from . import _lib
 from ._lib import HfVoteResult, check
 
+# libhetft kernel launches issued through this module (bench.py reports the
+# count inside its timed region as gpu_launches)
+LAUNCHES = 0
+
+
+def _count(n: int = 1) -> None:
+    global LAUNCHES
+    LAUNCHES += n
+
 _TORCH_DTYPE = {
     torch.float32: _lib.HF_F32,
     torch.float64: _lib.HF_F64,
@@ -120,6 +129,7 @@ def vote(replicas: Sequence[torch.Tensor], rel_tol=0.001, ulp_tol=None,
                      voted.data_ptr() if voted is not None else None, ctypes.byref(out),
                      device, _stream_ptr(device, stream))
     check("hf_vote", rc)
+    _count()
     return VoteResult.from_c(out)
 
 
@@ -139,6 +149,7 @@ def vote_bytes(replicas: Sequence[torch.Tensor], elem_width: int,
                                    voted.data_ptr() if voted is not None else None,
                                    ctypes.byref(out), device, _stream_ptr(device, stream))
     check("hf_vote_bytes", rc)
+    _count()
     return VoteResult.from_c(out)
 
 
@@ -172,6 +183,7 @@ def vote_async(replicas: Sequence[torch.Tensor], ws: VoteWorkspace, rel_tol=0.00
                                    ws.result.data_ptr(), ws.ws.data_ptr(), ws.device,
                                    _stream_ptr(ws.device, stream))
     check("hf_vote_async", rc)
+    _count()
 
 
 # ---- copy / checkpoint ------------------------------------------------------
@@ -194,6 +206,15 @@ def copy(dst: torch.Tensor, src: torch.Tensor, stream: Optional[torch.cuda.Strea
     sdev = dd if dd >= 0 else sd
     check("hf_copy", _lib.load().hf_copy(dst.data_ptr(), dd, src.data_ptr(), sd, nb,
                                          _stream_ptr(sdev, stream) if sdev >= 0 else None))
+    if dd >= 0 and sd >= 0 and (dd == sd or _lib.peer_enabled(dd, sd)):
+        _count()        # copy kernel (host <-> device goes to the copy engine)
+
+
+def fill(dst: torch.Tensor, value: int = 0, stream: Optional[torch.cuda.Stream] = None) -> None:
+    _lib.init()
+    d = _loc(dst)
+    check("hf_fill", _lib.load().hf_fill(dst.data_ptr(), int(value), _nbytes(dst), d,
+                                         _stream_ptr(d, stream) if d >= 0 else None))
 
 
 def checkpoint(ckpt: torch.Tensor, buf: torch.Tensor, with_checksum: bool = False,
@@ -207,6 +228,7 @@ def checkpoint(ckpt: torch.Tensor, buf: torch.Tensor, with_checksum: bool = Fals
     check("hf_checkpoint", _lib.load().hf_checkpoint(
         ckpt.data_ptr(), buf.data_ptr(), nb, ctypes.byref(cs) if with_checksum else None, dev,
         _stream_ptr(dev, stream)))
+    _count()
     return int(cs.value) if with_checksum else None
 
 
@@ -221,6 +243,7 @@ def restore(buf: torch.Tensor, ckpt: torch.Tensor, expect: Optional[int] = None,
     check("hf_restore", _lib.load().hf_restore(buf.data_ptr(), ckpt.data_ptr(), nb,
                                                ctypes.byref(ex) if ex is not None else None, dev,
                                                _stream_ptr(dev, stream)))
+    _count()
 
 
 def checksum(buf: torch.Tensor, stream: Optional[torch.cuda.Stream] = None) -> int:
@@ -229,33 +252,52 @@ def checksum(buf: torch.Tensor, stream: Optional[torch.cuda.Stream] = None) -> i
     out = ctypes.c_uint64(0)
     check("hf_checksum", _lib.load().hf_checksum(buf.data_ptr(), _nbytes(buf), ctypes.byref(out),
                                                  dev, _stream_ptr(dev, stream)))
+    _count()
     return int(out.value)
 
 
 # ---- fault injection ----------------------------------------------------------
 
-def inject_bitflip(buf: torch.Tensor, elem: int, bit: int,
-                   stream: Optional[torch.cuda.Stream] = None) -> None:
+def _inj_dev(buf: torch.Tensor, device: Optional[int]) -> int:
+    # pinned host buffers are device-visible through UVA; the kernel then runs
+    # on `device` (default GPU 0) and writes the host bytes in place
+    if buf.device.type == "cuda":
+        return _dev(buf)
+    return 0 if device is None else device
+
+
+def inject_bitflip(buf: torch.Tensor, elem: int, bit: int, stream: Optional[torch.cuda.Stream] = None,
+                   device: Optional[int] = None) -> None:
     _lib.init()
-    dev = _dev(buf)
+    dev = _inj_dev(buf, device)
     check("hf_inject_bitflip", _lib.load().hf_inject_bitflip(
         buf.data_ptr(), hf_dtype(buf), int(elem), int(bit), dev, _stream_ptr(dev, stream)))
+    _count()
+    if buf.device.type != "cuda":
+        torch.cuda.synchronize(dev)
 
 
-def inject_scale(buf: torch.Tensor, elem: int, rel: float,
-                 stream: Optional[torch.cuda.Stream] = None) -> None:
+def inject_scale(buf: torch.Tensor, elem: int, rel: float, stream: Optional[torch.cuda.Stream] = None,
+                 device: Optional[int] = None) -> None:
     _lib.init()
-    dev = _dev(buf)
+    dev = _inj_dev(buf, device)
     check("hf_inject_scale", _lib.load().hf_inject_scale(
         buf.data_ptr(), hf_dtype(buf), int(elem), float(rel), dev, _stream_ptr(dev, stream)))
+    _count()
+    if buf.device.type != "cuda":
+        torch.cuda.synchronize(dev)
 
 
-def scribble(buf: torch.Tensor, data: bytes, stream: Optional[torch.cuda.Stream] = None) -> None:
+def scribble(buf: torch.Tensor, data: bytes, stream: Optional[torch.cuda.Stream] = None,
+             device: Optional[int] = None) -> None:
     _lib.init()
-    dev = _dev(buf)
+    dev = _inj_dev(buf, device)
     raw = (ctypes.c_uint8 * max(1, len(data)))(*data)
     check("hf_scribble", _lib.load().hf_scribble(buf.data_ptr(), raw, len(data), dev,
                                                  _stream_ptr(dev, stream)))
+    _count()
+    if buf.device.type != "cuda":
+        torch.cuda.synchronize(dev)
 
 
 # ---- matmul variants -------------------------------------------------------------
@@ -282,6 +324,8 @@ def gemm_simt(A: torch.Tensor, B: torch.Tensor, C: torch.Tensor,
     dev = _dev(C)
     check("hf_gemm_simt", _lib.load().hf_gemm_simt(A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K,
                                                    dev, _stream_ptr(dev, stream)))
+    fast = M % 128 == 0 and N % 128 == 0 and K % 32 == 0
+    _count(2 if fast else 1)    # transpose pre-pass + sgemm
 
 
 def gemm_tc(A: torch.Tensor, B: torch.Tensor, C: torch.Tensor, mode: int = _lib.HF_GEMM_TF32,
@@ -291,3 +335,4 @@ def gemm_tc(A: torch.Tensor, B: torch.Tensor, C: torch.Tensor, mode: int = _lib.
     dev = _dev(C)
     check("hf_gemm_tc", _lib.load().hf_gemm_tc(A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K,
                                                mode, dev, _stream_ptr(dev, stream)))
+    _count(3)           # B^T (+split) pre-pass, A round/split, tcgen05 GEMM

@@ -1,0 +1,238 @@
+"""Heterogeneity-aware result voting — the voter interface of
+/root/reference/pkg/src/hetrt/voting.py (paper §IV-D) kept as the drop-in,
+with the element-wise comparison running in the hf_vote sm_100a kernel.
+
+Kept: VoterKernelProfile / default_voter_profiles / VoterConfig (δ = 0.1 %
+default) / VoteOutcome / compare / compare_payloads / voter_cost_ns /
+VoterPlacement / place_voter, with the reference's area ordering, error
+behaviour and K = 2 verdict + first divergence (voting.py:58-174).
+
+New: K-replica majority voting with per-replica
+mismatch counts, winner, unresolved count and a voted buffer; per-variant
+(per-kernel) relative tolerances and an optional ULP rule; a measured B200
+voter profile (hf_vote: ~launch + sync latency, per byte 1/HBM rate).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from .devices import Fleet, ValueType
+from .errors import DispatchError
+
+
+@dataclass
+class VoterKernelProfile:
+    kernel: str
+    unit_kind: str
+    base_ns: int
+    per_byte_ns: float
+
+    def cost_ns(self, size_bytes: int) -> int:
+        return max(1, round(self.base_ns + self.per_byte_ns * size_bytes))
+
+
+# hf_vote on a B200: ~10 us launch+sync floor, (K+1)·n bytes at ~6 TB/s; the
+# profile is per compared byte (K·n), so 1/6000 ns per byte is a lower bound
+B200_VOTER_BASE_NS = 10_000
+B200_VOTER_NS_PER_BYTE = 1.0 / 6000.0
+
+
+def default_voter_profiles(gpu_kinds: Sequence[str] = ("gpu-tc", "gpu-simt")) -> list:
+    """The reference calibration (voting.py:37-42) plus hf_vote on B200 unit kinds."""
+    profiles = [
+        VoterKernelProfile("voter_single", "cpu", 1_000, 1.0),
+        VoterKernelProfile("voter_parallel", "cpu", 10_000, 0.1),
+        VoterKernelProfile("voter_gpu", "gpu", 19_000, 0.001),
+    ]
+    profiles += [VoterKernelProfile("hf_vote", k, B200_VOTER_BASE_NS, B200_VOTER_NS_PER_BYTE) for k in gpu_kinds]
+    return profiles
+
+
+@dataclass
+class VoterConfig:
+    float_delta: float = 0.001
+    placement: str = "lowest-F"
+    profiles: list = field(default_factory=default_voter_profiles)
+    kernel_delta: dict = field(default_factory=dict)   # per-variant δ (kernel -> δ)
+    ulp_tolerance: Optional[int] = None                # float pairs also agree within N ulps
+
+    def __post_init__(self):
+        if self.float_delta < 0:
+            raise ValueError(f"float_delta must be >= 0, got {self.float_delta}")
+        if self.placement not in ("lowest-F", "avoid-task-units"):
+            raise ValueError(f"unknown voter placement {self.placement!r}")
+        for k, d in self.kernel_delta.items():
+            if d < 0:
+                raise ValueError(f"kernel_delta[{k!r}] must be >= 0, got {d}")
+
+    def delta_for(self, kernel: Optional[str], task_delta: Optional[float] = None) -> float:
+        base = self.float_delta if task_delta is None else task_delta
+        return self.kernel_delta.get(kernel, base) if kernel is not None else base
+
+
+@dataclass
+class VoteOutcome:
+    """verdict: "match" | "mismatch" (K = 2, reference) plus "corrected"
+    (K >= 3: a majority exists for every element, some replica differs).
+    first_divergence: (area, index, value_a, value_b) for K = 2 (reference),
+    (area, index, (value_0, ..., value_{K-1})) for K >= 3."""
+
+    verdict: str
+    first_divergence: Optional[tuple] = None
+    mismatch: list = field(default_factory=list)
+    unresolved: int = 0
+    winner: int = 0
+    per_area: dict = field(default_factory=dict)
+    vote_ns: int = 0
+
+    @property
+    def is_match(self) -> bool:
+        return self.verdict == "match"
+
+    @property
+    def committed(self) -> bool:
+        return self.verdict in ("match", "corrected")
+
+    @property
+    def faulty(self) -> list:
+        return [r for r, m in enumerate(self.mismatch) if m > 0]
+
+
+def _element(raw: bytes, vt: ValueType, width: int, idx: int):
+    if vt.numpy_dtype is not None:
+        return float(np.frombuffer(raw, dtype=vt.numpy_dtype, count=1, offset=idx * width)[0])
+    return bytes(raw[idx * width:(idx + 1) * width])
+
+
+_BACKEND = None
+
+
+def _default_backend():
+    global _BACKEND
+    if _BACKEND is None:
+        from .backend import CudaBackend
+        _BACKEND = CudaBackend()
+    return _BACKEND
+
+
+def compare_payloads(a: bytes, b: bytes, value_type: ValueType, elem_width: int, delta: float, backend=None):
+    """First diverging element of one area's two payloads, or None
+    (voting.py:84-103), computed by hf_vote on the GPU."""
+    if len(a) != len(b):
+        raise DispatchError(f"result payloads differ in size: {len(a)} vs {len(b)} bytes")
+    be = backend or _default_backend()
+    host = _host_space()
+    bufs = [be.from_bytes(host, a), be.from_bytes(host, b)]
+    res, _ = be.vote(bufs, value_type, elem_width, [delta, delta])
+    if res.first_div < 0:
+        return None
+    i = res.first_div
+    return i, _element(a, value_type, elem_width, i), _element(b, value_type, elem_width, i)
+
+
+def _host_space():
+    from .devices import MemorySpace
+    return MemorySpace("host", is_host=True)
+
+
+def compare(result_a: dict, result_b: dict, config: VoterConfig, backend=None) -> VoteOutcome:
+    """Reference compare (voting.py:106-123): two result sets keyed by area
+    id, values (payload bytes, value type, element width); areas in sorted
+    order, the first mismatching area decides."""
+    if set(result_a) != set(result_b):
+        raise DispatchError(f"result sets cover different areas: {sorted(result_a)} vs {sorted(result_b)}")
+    for area in sorted(result_a):
+        pa, vt_a, w_a = result_a[area]
+        pb, vt_b, w_b = result_b[area]
+        if vt_a is not vt_b or w_a != w_b:
+            raise DispatchError(f"area {area!r}: value type mismatch between results")
+        div = compare_payloads(bytes(pa), bytes(pb), vt_a, w_a, config.float_delta, backend)
+        if div is not None:
+            idx, va, vb = div
+            return VoteOutcome("mismatch", (area, idx, va, vb), [1, 1], 1, 0)
+    return VoteOutcome("match", None, [0, 0], 0, 0)
+
+
+def vote_buffers(backend, areas: Sequence[tuple], rel_tols: Sequence[float], ulp: Optional[int] = None,
+                 device: Optional[int] = None, in_place: bool = True) -> VoteOutcome:
+    """K-way vote over device/host buffers.
+
+    areas: (area id, [K buffers], value type, width) in any order; they are
+    voted in sorted area order (reference rule).  With in_place the voted
+    output is written over replica 0's buffer (the kernel only stores
+    elements whose voted value differs from replica 0), so committing
+    replica 0's handles commits the voted result."""
+    areas = sorted(areas, key=lambda a: a[0])
+    K = len(areas[0][1]) if areas else 0
+    total = [0] * K
+    unresolved = 0
+    first = None
+    per_area = {}
+    vote_ns = 0
+    for area, bufs, vt, width in areas:
+        if len(bufs) != K:
+            raise DispatchError(f"area {area!r}: {len(bufs)} replicas, expected {K}")
+        ulps = None if ulp is None or vt.numpy_dtype is None else [ulp] * K
+        res, ns = backend.vote(bufs, vt, width, list(rel_tols), ulps,
+                               voted=bufs[0] if (in_place and K >= 3) else None, device=device)
+        vote_ns += ns
+        per_area[area] = res
+        total = [t + m for t, m in zip(total, res.mismatch)]
+        unresolved += res.unresolved
+        if first is None and res.first_div >= 0:
+            raws = [backend.element_bytes(b, res.first_div, width) for b in bufs]
+            vals = [_element(r, vt, width, 0) for r in raws]
+            first = (area, res.first_div, vals[0], vals[1]) if K == 2 else (area, res.first_div, tuple(vals))
+    if unresolved:
+        verdict = "mismatch"
+    elif any(total):
+        verdict = "corrected"
+    else:
+        verdict = "match"
+    winner = min(range(K), key=lambda r: (total[r], r)) if K else 0
+    return VoteOutcome(verdict, first, total, unresolved, winner, per_area, vote_ns)
+
+
+def voter_cost_ns(config: VoterConfig, unit_kind: str, size_bytes: int) -> int:
+    costs = [p.cost_ns(size_bytes) for p in config.profiles if p.unit_kind == unit_kind]
+    if not costs:
+        raise DispatchError(f"no voter kernel for unit kind {unit_kind!r}")
+    return min(costs)
+
+
+@dataclass
+class VoterPlacement:
+    kernel: str
+    unit_id: str
+    compute_ns: int
+    transfer_ns: int
+
+    @property
+    def total_ns(self) -> int:
+        return self.compute_ns + self.transfer_ns
+
+
+def place_voter(fleet: Fleet, config: VoterConfig, results: Sequence[tuple],
+                task_units: Sequence[str] = ()) -> VoterPlacement:
+    """Cheapest (voter kernel, unit): compare cost plus shipping every replica
+    copy into the voter's space (voting.py:146-174, generalised to K copies:
+    `results` rows are (n_bytes, space_0, ..., space_{K-1}))."""
+    size = sum(r[0] for r in results)
+    cands = []
+    for prof in config.profiles:
+        for unit in fleet.units.values():
+            if unit.kind != prof.unit_kind:
+                continue
+            ship = sum(fleet.transfers.cost_ns(sp, unit.memory_space, row[0]) for row in results for sp in row[1:])
+            cands.append(VoterPlacement(prof.kernel, unit.id, prof.cost_ns(size), ship))
+    if not cands:
+        raise DispatchError("no voter-capable unit in the fleet")
+    if config.placement == "avoid-task-units":
+        outside = [c for c in cands if c.unit_id not in set(task_units)]
+        if outside:
+            cands = outside
+    return min(cands, key=lambda c: (c.total_ns, c.unit_id, c.kernel))

@@ -1,0 +1,151 @@
+"""Built-in tasks and their diverse kernel variants.
+
+``matmul`` is the north-star workload: C = A·B on fp32 n x n operands with
+three diverse GPU variants, attached per unit kind like the paper's
+OpenMP/CUDA pair (§IV-D; reference registry workloads.py:61-111):
+  mm_tc     "gpu-tc"    tcgen05.mma kind::tf32, RN-rounded operands
+  mm_simt   "gpu-simt"  register-tiled FP32 FFMA (no tensor cores)
+  mm_tc3x   "gpu-tc3"   tcgen05 3xTF32 (hi/lo split) — a third, numerically
+                        distinct variant for single-GPU TMR
+The reference's 1-D tasks (inc, pathfinder-like, buggy-inc; workloads.py:25-58)
+keep their CPU bodies (numpy over pinned host views) and get GPU bodies that
+run on device views, so the reference experiments stay runnable.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Callable, Optional
+
+import numpy as np
+
+from .api import Param
+from .errors import WorkloadError
+
+
+def _is_numpy(x) -> bool:
+    return isinstance(x, np.ndarray)
+
+
+# ---- matmul ------------------------------------------------------------------
+
+def _mm_views(ctx):
+    n = int(ctx.arg("n"))
+    a = ctx.request("A", "r").view(n, n)
+    b = ctx.request("B", "r").view(n, n)
+    c = ctx.request("C", "w").view(n, n)
+    return a, b, c
+
+
+def mm_tc_body(ctx):
+    from . import kernels
+    a, b, c = _mm_views(ctx)
+    kernels.gemm_tc(a, b, c, mode=0, stream=ctx.stream)
+
+
+def mm_tc3x_body(ctx):
+    from . import kernels
+    a, b, c = _mm_views(ctx)
+    kernels.gemm_tc(a, b, c, mode=1, stream=ctx.stream)
+
+
+def mm_simt_body(ctx):
+    from . import kernels
+    a, b, c = _mm_views(ctx)
+    kernels.gemm_simt(a, b, c, stream=ctx.stream)
+
+
+MATMUL_PARAMS = (Param.area("A", "r"), Param.area("B", "r"), Param.area("C", "w"), Param.scalar("n"))
+MATMUL_VARIANTS = (("mm_tc", "gpu-tc", mm_tc_body), ("mm_simt", "gpu-simt", mm_simt_body),
+                   ("mm_tc3x", "gpu-tc3", mm_tc3x_body))
+
+
+# ---- reference 1-D tasks ---------------------------------------------------------------
+
+def _inc_body(ctx):
+    n = ctx.arg("count")
+    src = ctx.request("input", "r")
+    dst = ctx.request("output", "w")
+    if _is_numpy(src):
+        np.add(src[:n], np.float32(1.0), out=dst[:n])
+    else:
+        dst[:n].copy_(src[:n]).add_(1.0)
+
+
+def _path_body(ctx):
+    n = ctx.arg("count")
+    src = ctx.request("input", "r")
+    dst = ctx.request("output", "w")
+    a = src[:n]
+    if _is_numpy(a):
+        left = np.concatenate((a[:1], a[:-1]))
+        right = np.concatenate((a[1:], a[-1:]))
+        np.add(a, np.minimum(np.minimum(left, a), right), out=dst[:n])
+    else:
+        import torch
+        left = torch.cat((a[:1], a[:-1]))
+        right = torch.cat((a[1:], a[-1:]))
+        torch.add(a, torch.minimum(torch.minimum(left, a), right), out=dst[:n])
+
+
+def _buggy_inc_body(ctx):
+    # off-by-one loop bound: the last element is never written
+    n = ctx.arg("count")
+    src = ctx.request("input", "r")
+    dst = ctx.request("output", "w")
+    if _is_numpy(src):
+        np.add(src[:n - 1], np.float32(1.0), out=dst[:n - 1])
+    else:
+        dst[:n - 1].copy_(src[:n - 1]).add_(1.0)
+
+
+@dataclass
+class Workload:
+    name: str
+    description: str
+    variants: list                                   # (kernel id, unit kind, body)
+    params: tuple = field(default_factory=lambda: (Param.area("input", "r"), Param.area("output", "w"),
+                                                   Param.scalar("count")))
+    make_input: Optional[Callable] = None
+
+    def attach(self, runtime, float_delta: Optional[float] = None, kinds=None):
+        task = runtime.declare_task(self.name, self.params, float_delta=float_delta)
+        for kernel, kind, body in self.variants:
+            if kinds is None or kind in kinds:
+                runtime.attach_kernel(task, kernel, kind, body)
+        return task
+
+
+def _uniform_input(size: int, rng) -> np.ndarray:
+    """U[1,2) fp32 (the reference's input distribution, workloads.py:70-72)."""
+    return np.asarray([rng.uniform(1.0, 2.0) for _ in range(size)], dtype=np.float32)
+
+
+_REGISTRY: dict = {}
+
+
+def _register(w: Workload) -> Workload:
+    _REGISTRY[w.name] = w
+    return w
+
+
+_register(Workload("inc", "increment an array of floats; identical math on every unit kind",
+                   [("inc_cpu", "cpu", _inc_body), ("inc_gpu", "gpu", _inc_body)], make_input=_uniform_input))
+_register(Workload("pathfinder-like", "neighborhood-minimum reduction",
+                   [("path_cpu", "cpu", _path_body), ("path_gpu", "gpu", _path_body)], make_input=_uniform_input))
+_register(Workload("buggy-inc", "increment with a deterministic off-by-one bug in the GPU variant",
+                   [("inc_ref_cpu", "cpu", _inc_body), ("inc_buggy_gpu", "gpu", _buggy_inc_body)],
+                   make_input=_uniform_input))
+_register(Workload("matmul", "C = A·B, fp32 n x n: tcgen05 TF32 / SIMT FP32 / tcgen05 3xTF32 variants",
+                   list(MATMUL_VARIANTS), params=MATMUL_PARAMS))
+
+
+def builtin_workloads() -> dict:
+    return dict(_REGISTRY)
+
+
+def get_workload(name: str) -> Workload:
+    try:
+        return _REGISTRY[name]
+    except KeyError:
+        raise WorkloadError(f"unknown workload {name!r}; available: {', '.join(sorted(_REGISTRY))}") from None

@@ -1,0 +1,159 @@
+"""End-to-end GPU tests of the drop-in Runtime: duplicated execution of the
+matmul variants, K-way voting, device checkpoint/rollback and seeded fault
+injection, checked against the CPU oracle.
+
+The fault-schedule parity test replays every round the executor ran with
+the oracle's restatement of the reference draw order (oracle/fault_schedule.py)
+and the oracle voter, and requires identical verdicts, per-replica mismatch
+counts and first divergences (bit-exact decisions)."""
+
+import random
+
+import numpy as np
+import pytest
+
+from oracle import fault_schedule
+from oracle import matmul as omatmul
+from oracle import vote as ovote
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+import paper_1405_2912_b200 as hf  # noqa: E402
+from paper_1405_2912_b200 import kernels  # noqa: E402
+
+
+def matmul_runtime(kinds=("gpu-tc", "gpu-simt"), overrides=None, **cfg_kw):
+    cfg = hf.gpu_fleet_config(devices=(0,), kinds=kinds)
+    cfg["memory_spaces"].append({"id": "gpu0ckpt", "device": 0})
+    for u in cfg["units"]:
+        u.update((overrides or {}).get(u["id"], {}))
+    rt = hf.Runtime(hf.load_fleet(cfg), hf.RuntimeConfig(**cfg_kw))
+    task = hf.get_workload("matmul").attach(rt, kinds=kinds)
+    return rt, task
+
+
+def register_mm(rt, a, b, device_inputs=False):
+    n = a.shape[0]
+    vt = hf.ValueType.FLOAT32
+    if device_inputs:
+        ia = rt.register_device_data(torch.from_numpy(a).cuda().view(-1).view(torch.uint8), n * n, vt, "r", "gpu0mem")
+        ib = rt.register_device_data(torch.from_numpy(b).cuda().view(-1).view(torch.uint8), n * n, vt, "r", "gpu0mem")
+    else:
+        ia = rt.register_data(a.tobytes(), n * n, vt, "r")
+        ib = rt.register_data(b.tobytes(), n * n, vt, "r")
+    ic = rt.register_data(bytes(4 * n * n), n * n, vt, "w")
+    return ia, ib, ic, {"A": ia, "B": ib, "C": ic, "n": n}
+
+
+def test_dmr_matmul_fault_free_matches_oracle():
+    a, b = omatmul.make_inputs(512, seed=3)
+    rt, task = matmul_runtime()
+    _, _, ic, args = register_mm(rt, a, b)
+    rep = rt.invoke(task, args, hf.Strategy(hf.StrategyKind.HET_DMR))
+    assert rep.success and rep.votes == ["match"]
+    got = rt.read_array(ic).reshape(512, 512)
+    assert ovote.reference_first_divergence(got.reshape(-1), omatmul.matmul(a, b).reshape(-1), 1e-3) is None
+    assert {s for s in rep.rounds_log[0]["slots"]} == {"gpu0.simt", "gpu0.tc"}
+
+
+def test_dmr_detects_corruption_and_reruns():
+    a, b = omatmul.make_inputs(256, seed=4)
+    # find a seed whose first draw is corrupt and second is clean at p = 0.5
+    seed = next(s for s in range(100) if random.Random(s).random() < 0.5 and
+                (lambda r: (r.random(), r.randrange(1), r.randrange(256 * 256), r.random())[3])(random.Random(s)) >= 0.5)
+    rt, task = matmul_runtime(overrides={"gpu0.tc": {"corrupt_prob": 0.5, "seed": seed,
+                                                     "corrupt_rel_magnitude": 0.5}})
+    _, _, ic, args = register_mm(rt, a, b)
+    rep = rt.invoke(task, args, hf.Strategy(hf.StrategyKind.HET_DMR))
+    assert rep.success
+    assert rep.votes == ["mismatch", "match"]
+    assert rep.fault_counts["vote_mismatch"] == 1
+    got = rt.read_array(ic)
+    assert ovote.reference_first_divergence(got, omatmul.matmul(a, b).reshape(-1), 1e-3) is None
+
+
+def test_tmr_majority_corrects_single_faulty_variant():
+    a, b = omatmul.make_inputs(256, seed=5)
+    rt, task = matmul_runtime(kinds=("gpu-tc", "gpu-simt", "gpu-tc3"),
+                              overrides={"gpu0.tc": {"corrupt_prob": 1.0, "corrupt_rel_magnitude": 0.5}})
+    _, _, ic, args = register_mm(rt, a, b)
+    rep = rt.invoke(task, args, hf.Strategy(hf.StrategyKind.HET_TMR))
+    assert rep.success and rep.votes == ["corrected"]
+    log = rep.rounds_log[0]
+    faulty_slot = log["slots"].index("gpu0.tc")
+    assert log["mismatch"][faulty_slot] == 1 and sum(log["mismatch"]) == 1
+    # the committed result is the voted buffer: never the corrupted element
+    got = rt.read_array(ic)
+    ref = omatmul.matmul(a, b).reshape(-1)
+    assert ovote.reference_first_divergence(got, ref, 1e-3) is None
+    # the faulty unit's reliability rating was penalised
+    rec = rt.profiles.record(rt.profiles.key_for("mm_tc", 256 * 256, "gpu0.tc"))
+    assert rec.t - rec.v == 1
+
+
+def test_perfcp_abort_rolls_back_to_hbm_checkpoint():
+    a, b = omatmul.make_inputs(256, seed=6)
+    rt, task = matmul_runtime(overrides={"gpu0.simt": {"abort_prob": 1.0}}, checkpoint_space="gpu0ckpt")
+    ia, ib, ic, args = register_mm(rt, a, b, device_inputs=True)
+    rep = rt.invoke(task, args, hf.Strategy(hf.StrategyKind.PERF_CP))
+    assert rep.success and rep.fault_counts["abort"] >= 1
+    # inputs were sole device copies: protected attempts snapshot them into HBM
+    assert rt.memory.checkpoints >= 2
+    table = rt.memory.sibling_table()
+    assert (ia, "gpu0ckpt", 0, True) in table
+    got = rt.read_array(ic)
+    assert ovote.reference_first_divergence(got, omatmul.matmul(a, b).reshape(-1), 1e-3) is None
+
+
+COPY_PARAMS = (hf.Param.area("input", "r"), hf.Param.area("output", "w"), hf.Param.scalar("count"))
+
+
+def _copy_body(ctx):
+    kernels.copy(ctx.request("output", "w"), ctx.request("input", "r"), stream=ctx.stream)
+
+
+@pytest.mark.parametrize("K,strategy", [(2, hf.StrategyKind.HET_DMR), (3, hf.StrategyKind.HET_TMR)])
+def test_fault_schedule_and_decisions_match_oracle(K, strategy):
+    """Seeded random bit flips on bit-identical replicas: every round's fault
+    placement and vote decision must equal the oracle replay."""
+    n = 4099
+    kinds = [f"gpu-v{i}" for i in range(K)]
+    cfg = {"memory_spaces": [{"id": "host", "host": True}, {"id": "gpu0mem", "device": 0}],
+           "units": [{"id": f"u{i}", "kind": kinds[i], "memory_space": "gpu0mem", "timing": "measured",
+                      "corrupt_prob": 0.35, "corrupt_mode": "bitflip", "seed": 100 + 7 * i} for i in range(K)]}
+    rt = hf.Runtime(hf.load_fleet(cfg), hf.RuntimeConfig(serial_replicas=True, attempt_limit=200))
+    task = rt.declare_task("copy", COPY_PARAMS)
+    for i in range(K):
+        rt.attach_kernel(task, f"copy{i}", kinds[i], _copy_body)
+    rng = np.random.default_rng(0)
+    oracle_rngs = {f"u{i}": random.Random(100 + 7 * i) for i in range(K)}
+    rounds = 0
+    for t in range(25):
+        data = rng.uniform(1, 2, n).astype(np.float32)
+        inp = rt.register_data(data.tobytes(), n, hf.ValueType.FLOAT32, "r")
+        out = rt.register_data(bytes(4 * n), n, hf.ValueType.FLOAT32, "w")
+        rep = rt.invoke(task, {"input": inp, "output": out, "count": n}, hf.Strategy(strategy))
+        for log in rep.rounds_log:
+            rounds += 1
+            reps = []
+            for slot, unit in sorted(log["launched"].items()):
+                view = data.copy()
+                ev = fault_schedule.apply_attempt(oracle_rngs[unit], (0, 0, 0, 0.35), [view], [True],
+                                                  mode="bitflip")
+                if ev["corrupt"] is not None:
+                    assert log["corrupt"][slot] == (ev["corrupt"][1], ev["corrupt"][2])
+                else:
+                    assert slot not in log["corrupt"]
+                reps.append(view)
+            if "verdict" in log:
+                ores = ovote.vote(reps, 1e-3)
+                expect = ores.verdict if K > 2 else ("match" if ores.verdict == "match" else "mismatch")
+                assert log["verdict"] == expect
+                assert log["mismatch"] == ores.mismatch
+                fd = log["first_divergence"]
+                assert (fd[1] if fd else -1) == ores.first_div
+        got = rt.read_array(out)
+        if rep.votes[-1] != "mismatch":
+            assert np.array_equal(got, data) or (K == 2)
+    assert rounds >= 25
