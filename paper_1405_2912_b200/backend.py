@@ -81,7 +81,11 @@ class CudaBackend:
             return lambda: dt
         ev = torch.cuda.Event(enable_timing=True)
         ev.record(stream)
-        return lambda: int(t0.elapsed_time(ev) * 1e6)
+
+        def elapsed() -> int:
+            ev.synchronize()
+            return int(t0.elapsed_time(ev) * 1e6)
+        return elapsed
 
     def is_device_error(self, exc: BaseException) -> bool:
         if isinstance(exc, _lib.HfError):
