@@ -290,17 +290,23 @@ def run_hetft_arm(args, rank, world, local):
             stats["attempt_ns"][k] = stats["attempt_ns"].get(k, 0) + int(f["duration_ns"])
             stats["attempt_n"][k] = stats["attempt_n"].get(k, 0) + 1
 
-    for _ in range(args.warmup):
+    # the clock sampler starts during warm-up (nvidia-smi needs ~0.5 s to
+    # emit its first sample) and stops right after the timed region
+    sampler = ClockSampler(device) if rank == 0 else None
+    device_step(False)
+    if sampler:
+        sampler.start()
+    t_start = time.perf_counter()
+    done = 1
+    while done < args.warmup or time.perf_counter() - t_start < 0.8:
         device_step(False)
+        done += 1
     torch.cuda.synchronize()
 
     # ---- timed region: device-resident inputs ----
     rt.executor._trace = on_trace
-    sampler = ClockSampler(device) if rank == 0 else None
     barrier()
     torch.cuda.synchronize()
-    if sampler:
-        sampler.start()
     launches0 = kernels.LAUNCHES
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)

@@ -49,6 +49,8 @@ def default_voter_profiles(gpu_kinds: Sequence[str] = ("gpu-tc", "gpu-simt")) ->
         VoterKernelProfile("voter_gpu", "gpu", 19_000, 0.001),
     ]
     profiles += [VoterKernelProfile("hf_vote", k, B200_VOTER_BASE_NS, B200_VOTER_NS_PER_BYTE) for k in gpu_kinds]
+    # "*": hf_vote on any unit that owns a CUDA device, whatever its kind
+    profiles.append(VoterKernelProfile("hf_vote", "*", B200_VOTER_BASE_NS, B200_VOTER_NS_PER_BYTE))
     return profiles
 
 
@@ -198,7 +200,7 @@ def vote_buffers(backend, areas: Sequence[tuple], rel_tols: Sequence[float], ulp
 
 
 def voter_cost_ns(config: VoterConfig, unit_kind: str, size_bytes: int) -> int:
-    costs = [p.cost_ns(size_bytes) for p in config.profiles if p.unit_kind == unit_kind]
+    costs = [p.cost_ns(size_bytes) for p in config.profiles if p.unit_kind == unit_kind and p.unit_kind != "*"]
     if not costs:
         raise DispatchError(f"no voter kernel for unit kind {unit_kind!r}")
     return min(costs)
@@ -225,7 +227,7 @@ def place_voter(fleet: Fleet, config: VoterConfig, results: Sequence[tuple],
     cands = []
     for prof in config.profiles:
         for unit in fleet.units.values():
-            if unit.kind != prof.unit_kind:
+            if unit.kind != prof.unit_kind and not (prof.unit_kind == "*" and unit.device is not None):
                 continue
             ship = sum(fleet.transfers.cost_ns(sp, unit.memory_space, row[0]) for row in results for sp in row[1:])
             cands.append(VoterPlacement(prof.kernel, unit.id, prof.cost_ns(size), ship))
