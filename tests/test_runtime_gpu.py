@@ -153,7 +153,8 @@ def test_fault_schedule_and_decisions_match_oracle(K, strategy):
                 assert log["mismatch"] == ores.mismatch
                 fd = log["first_divergence"]
                 assert (fd[1] if fd else -1) == ores.first_div
+        # committed output: exact unless an undetectable flip (within δ by
+        # definition) survived the vote
         got = rt.read_array(out)
-        if rep.votes[-1] != "mismatch":
-            assert np.array_equal(got, data) or (K == 2)
+        assert ovote.reference_first_divergence(got, data, 1e-3) is None
     assert rounds >= 25
