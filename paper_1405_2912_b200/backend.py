@@ -61,9 +61,48 @@ class CudaBackend:
                 self._streams[device] = s
         return s
 
+    def copy_stream(self, device: int):
+        """Second stream per device for host<->device traffic, so transfers
+        overlap kernels of the compute stream (copy engines are independent)."""
+        key = ("copy", device)
+        with self._lock:
+            s = self._streams.get(key)
+            if s is None:
+                s = torch.cuda.Stream(device=device)
+                self._streams[key] = s
+        return s
+
     def synchronize(self, stream) -> None:
         if stream is not None:
             stream.synchronize()
+
+    def record(self, stream):
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        return ev
+
+    def wait(self, stream, event) -> None:
+        """GPU-side dependency: `stream` waits for `event` (no host blocking)."""
+        if stream is not None and event is not None:
+            stream.wait_event(event)
+
+    def prefetch_copy(self, dst, dst_space: MemorySpace, src, src_space: MemorySpace):
+        """Asynchronous host->device copy on the destination's copy stream,
+        ordered after the compute stream's pending work; returns its event."""
+        dev = dst_space.device
+        cs = self.copy_stream(dev)
+        cs.wait_stream(self.stream(dev))
+        kernels.copy(dst, src, stream=cs)
+        return self.record(cs)
+
+    def readback_copy(self, dst_host, src, src_space: MemorySpace):
+        """Asynchronous device->host copy on the source's copy stream, ordered
+        after the compute stream's pending work; returns its event."""
+        dev = src_space.device
+        cs = self.copy_stream(dev)
+        cs.wait_stream(self.stream(dev))
+        kernels.copy(dst_host, src, stream=cs)
+        return self.record(cs)
 
     def timer_start(self, stream, device):
         if stream is None:

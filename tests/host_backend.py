@@ -37,6 +37,23 @@ class HostBackend:
     def stream(self, device):
         return None
 
+    def copy_stream(self, device):
+        return None
+
+    def record(self, stream):
+        return None
+
+    def wait(self, stream, event):
+        pass
+
+    def prefetch_copy(self, dst, dst_space, src, src_space):
+        dst[:] = src
+        return None
+
+    def readback_copy(self, dst_host, src, src_space):
+        dst_host[:] = src
+        return None
+
     def synchronize(self, stream):
         pass
 
