@@ -61,10 +61,11 @@ class CudaBackend:
                 self._streams[device] = s
         return s
 
-    def copy_stream(self, device: int):
-        """Second stream per device for host<->device traffic, so transfers
-        overlap kernels of the compute stream (copy engines are independent)."""
-        key = ("copy", device)
+    def copy_stream(self, device: int, direction: str = "h2d"):
+        """Extra streams per device for host<->device traffic, one per
+        direction (the copy engines are full duplex), so transfers overlap
+        the compute stream's kernels and each other."""
+        key = (direction, device)
         with self._lock:
             s = self._streams.get(key)
             if s is None:
@@ -99,7 +100,7 @@ class CudaBackend:
         """Asynchronous device->host copy on the source's copy stream, ordered
         after the compute stream's pending work; returns its event."""
         dev = src_space.device
-        cs = self.copy_stream(dev)
+        cs = self.copy_stream(dev, "d2h")
         cs.wait_stream(self.stream(dev))
         kernels.copy(dst_host, src, stream=cs)
         return self.record(cs)

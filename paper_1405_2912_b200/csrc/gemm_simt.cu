@@ -10,7 +10,10 @@
 // once by a tiled pre-pass (~2|A| bytes, ~1% of the GEMM) so both operands
 // stream as contiguous k-rows; 128x128x16 CTA tile, 256 threads, 8x8 outputs
 // per thread as 2x2 blocks of 4x4, cp.async 3-stage smem ring, one barrier
-// per k-tile, register double-buffered fragments, two CTAs per SM.  Warps are laid out 4x2 over the
+// per k-tile, register double-buffered fragments, two CTAs per SM; the
+// outer product issues packed FFMA2 (fma.rn.f32x2): every output is still an
+// fp32 FMA chain in ascending k, so results equal the FFMA formulation bit
+// for bit.  Warps are laid out 4x2 over the
 // 16x16 thread grid so each LDS.128 of A and of B is one wavefront.
 // Generic path: 16x16 bounds-checked tiles for ragged shapes.
 #include "common.cuh"
@@ -18,6 +21,18 @@
 namespace hf {
 
 constexpr int SB_M = 128, SB_N = 128, SB_K = 16, S_STAGES = 3;
+
+// Packed fp32x2 FMA (sm_100 FFMA2): two independent IEEE fp32 fused
+// multiply-adds with round-to-nearest per instruction — bit-identical to two
+// FFMAs, half the issue slots and register-port pressure.
+__device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void ffma2(unsigned long long& d, unsigned long long a, unsigned long long b) {
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
+}
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
@@ -79,11 +94,12 @@ sgemm_128x128(const float* __restrict__ At, const float* __restrict__ B, float* 
         cp_async16(bs + 8 * SB_N, Bg + kb + b8);
     };
 
-    float acc[8][8];
+    // acc[i][j] holds the output pair (2j, 2j+1) of row i
+    unsigned long long acc[8][4];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0ull;
 
     const int nk = K / SB_K;
 #pragma unroll
@@ -118,12 +134,15 @@ sgemm_128x128(const float* __restrict__ At, const float* __restrict__ B, float* 
             }
             const float a[8] = {fa[cur][0].x, fa[cur][0].y, fa[cur][0].z, fa[cur][0].w,
                                 fa[cur][1].x, fa[cur][1].y, fa[cur][1].z, fa[cur][1].w};
-            const float b[8] = {fb[cur][0].x, fb[cur][0].y, fb[cur][0].z, fb[cur][0].w,
-                                fb[cur][1].x, fb[cur][1].y, fb[cur][1].z, fb[cur][1].w};
+            // b pairs are the LDS.128 destination registers, already adjacent
+            const unsigned long long b[4] = {pack2(fb[cur][0].x, fb[cur][0].y), pack2(fb[cur][0].z, fb[cur][0].w),
+                                             pack2(fb[cur][1].x, fb[cur][1].y), pack2(fb[cur][1].z, fb[cur][1].w)};
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
+            for (int i = 0; i < 8; ++i) {
+                const unsigned long long ai = pack2(a[i], a[i]);   // folded into FFMA2's scalar operand
 #pragma unroll
-                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+                for (int j = 0; j < 4; ++j) ffma2(acc[i][j], ai, b[j]);
+            }
         }
     }
     cp_async_wait<0>();
@@ -132,9 +151,8 @@ sgemm_128x128(const float* __restrict__ At, const float* __restrict__ B, float* 
     for (int i = 0; i < 8; ++i) {
         const int row = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
         float* crow = C + static_cast<long long>(row) * N + n0;
-        *reinterpret_cast<float4*>(crow + tx * 4) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
-        *reinterpret_cast<float4*>(crow + 64 + tx * 4) =
-            make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+        *reinterpret_cast<ulonglong2*>(crow + tx * 4) = make_ulonglong2(acc[i][0], acc[i][1]);
+        *reinterpret_cast<ulonglong2*>(crow + 64 + tx * 4) = make_ulonglong2(acc[i][2], acc[i][3]);
     }
 }
 
