@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--fault-prob", type=float, default=0.05, help="per-replica corrupt (bit flip) probability")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--depth", type=int, default=1, help="TaskStream depth (tasks in flight beyond the one settling)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=12.0)
     return ap.parse_args()
@@ -263,24 +264,39 @@ def run_hetft_arm(args, rank, world, local):
     stats = {"tasks": 0, "rounds": 0, "votes": {}, "injected": 0, "mismatch": 0, "vote_ns": 0,
              "attempt_ns": {}, "attempt_n": {}}
 
-    def device_step(record: bool):
-        ia = rt.register_device_data(A, n * n, hf.ValueType.FLOAT32, "r", space)
-        ib = rt.register_device_data(B, n * n, hf.ValueType.FLOAT32, "r", space)
-        ic = rt.register_device_data(C0, n * n, hf.ValueType.FLOAT32, "w", space)
-        rep = rt.invoke(task, {"A": ia, "B": ib, "C": ic, "n": n}, strat)
-        if not rep.success:
-            raise RuntimeError("task failed")
-        if record:
-            stats["tasks"] += 1
-            stats["rounds"] += rep.rounds
-            for v in rep.votes:
-                stats["votes"][v] = stats["votes"].get(v, 0) + 1
-            stats["injected"] += len(rep.injected)
-            stats["mismatch"] += rep.fault_counts["vote_mismatch"]
-            stats["vote_ns"] += rep.voter_ns
-        for a in (ia, ib, ic):
-            rt.release(a)
-        return rep
+    def record(rep):
+        stats["tasks"] += 1
+        stats["rounds"] += rep.rounds
+        for v in rep.votes:
+            stats["votes"][v] = stats["votes"].get(v, 0) + 1
+        stats["injected"] += len(rep.injected)
+        stats["mismatch"] += rep.fault_counts["vote_mismatch"]
+        stats["vote_ns"] += rep.voter_ns
+
+    def device_stream(steps: int, recording: bool):
+        """`steps` voted tasks on device-resident inputs through a TaskStream:
+        task i+1's replicas are queued on the GPU before task i's verdict is
+        read, so host-side settling overlaps kernels."""
+        queue = []
+        with rt.task_stream(depth=args.depth) as ts:
+            for _ in range(steps):
+                ia = rt.register_device_data(A, n * n, hf.ValueType.FLOAT32, "r", space)
+                ib = rt.register_device_data(B, n * n, hf.ValueType.FLOAT32, "r", space)
+                ic = rt.register_device_data(C0, n * n, hf.ValueType.FLOAT32, "w", space)
+                queue.append((ts.submit(task, {"A": ia, "B": ib, "C": ic, "n": n}, strat), (ia, ib, ic)))
+                while queue and queue[0][0].success:
+                    rep, areas = queue.pop(0)
+                    if recording:
+                        record(rep)
+                    for x in areas:
+                        rt.release(x)
+        for rep, areas in queue:
+            if not rep.success:
+                raise RuntimeError("task failed")
+            if recording:
+                record(rep)
+            for x in areas:
+                rt.release(x)
 
     # trace per-kernel durations via the executor's measured attempts
     def on_trace(line: str):
@@ -293,14 +309,14 @@ def run_hetft_arm(args, rank, world, local):
     # the clock sampler starts during warm-up (nvidia-smi needs ~0.5 s to
     # emit its first sample) and stops right after the timed region
     sampler = ClockSampler(device) if rank == 0 else None
-    device_step(False)
+    device_stream(1, False)
     if sampler:
         sampler.start()
     t_start = time.perf_counter()
     done = 1
     while done < args.warmup or time.perf_counter() - t_start < 0.8:
-        device_step(False)
-        done += 1
+        device_stream(max(1, args.warmup), False)
+        done += max(1, args.warmup)
     torch.cuda.synchronize()
 
     # ---- timed region: device-resident inputs ----
@@ -310,8 +326,7 @@ def run_hetft_arm(args, rank, world, local):
     launches0 = kernels.LAUNCHES
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    for _ in range(args.steps):
-        device_step(True)
+    device_stream(args.steps, True)
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -340,25 +355,30 @@ def run_hetft_arm(args, rank, world, local):
         return ia, ib, ic
 
     def host_stream(steps):
-        """Software pipeline over the public API: step i+1's inputs go H2D and
-        step i-1's result goes D2H on the copy engines while step i computes."""
+        """Software pipeline over the public API: step i+1's inputs go H2D on
+        the copy engine and step i-1's result goes D2H while step i computes;
+        a TaskStream keeps the next task's kernels queued behind the current."""
         nxt = stage(0)
-        last = None
-        retired = ()
-        for i in range(steps):
-            ia, ib, ic = nxt
-            if i + 1 < steps:
-                nxt = stage(i + 1)
-            rt.invoke(task, {"A": ia, "B": ib, "C": ic, "n": n}, strat)
-            last = rt.read_into_async(ic, hC)
-            # release step i-1 only now: its D2H overlapped step i's kernels
-            for a in retired:
-                rt.release(a)
-            retired = (ia, ib, ic)
+        queue, retired, last = [], [], None
+        with rt.task_stream(depth=args.depth) as ts:
+            for i in range(steps):
+                ia, ib, ic = nxt
+                if i + 1 < steps:
+                    nxt = stage(i + 1)
+                queue.append((ts.submit(task, {"A": ia, "B": ib, "C": ic, "n": n}, strat), (ia, ib, ic)))
+                while queue and queue[0][0].success:
+                    rep, areas = queue.pop(0)
+                    last = rt.read_into_async(areas[2], hC)
+                    for x in retired:     # released one step late: their D2H overlapped
+                        rt.release(x)
+                    retired = list(areas)
+        for rep, areas in queue:
+            last = rt.read_into_async(areas[2], hC)
+            retired += list(areas)
         if last is not None:
             last.synchronize()
-        for a in retired:
-            rt.release(a)
+        for x in retired:
+            rt.release(x)
 
     host_stream(2)
     torch.cuda.synchronize()

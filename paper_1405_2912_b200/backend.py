@@ -48,6 +48,8 @@ class CudaBackend:
         self._streams: dict = {}
         self._lock = threading.Lock()
         self.launches = 0             # libhetft kernel launches issued through this backend
+        self.slice_across_gpus = True  # replicas on >= 2 GPUs: sliced vote
+        self._vote_slots: dict = {}
 
     # -- streams / timing ---------------------------------------------------------
 
@@ -234,20 +236,79 @@ class CudaBackend:
 
     # -- voting -----------------------------------------------------------------------
 
+    def vote_start(self, bufs: Sequence, value_type: ValueType, width: int, rel_tol, ulp_tol=None,
+                   voted=None, device: Optional[int] = None):
+        """Launch a vote without waiting: hf_vote_async into a pooled device
+        workspace, then an async 96-byte D2H of the result on the same stream.
+        Replicas on several GPUs use the sliced path (synchronous)."""
+        devs = []
+        for b in bufs:
+            if b.device.type == "cuda" and b.device.index not in devs:
+                devs.append(b.device.index)
+        typed = value_type.numpy_dtype is not None or width in INT_DTYPES
+        if not typed or (self.slice_across_gpus and len(devs) >= 2) or not devs:
+            from .voting import DoneVote
+            return DoneVote(*self.vote(bufs, value_type, width, rel_tol, ulp_tol, voted, device))
+        if device is None:
+            device = devs[0]
+        st = self.stream(device)
+        for d in devs:
+            if d != device:
+                st.wait_stream(self.stream(d))
+        slot = self._vote_slot(device)
+        start = self.timer_start(st, device)
+        dt = torch_dtype(view_dtype(value_type, width))
+        kernels.vote_async([b.view(dt) for b in bufs], slot.ws, rel_tol, ulp_tol,
+                           voted=voted.view(dt) if voted is not None else None, stream=st)
+        kernels.copy(slot.host, slot.ws.result, stream=st)
+        stop = self.timer_stop(start, st, device)
+        self.launches += 1
+        return _PendingVote(self, slot, device, stop)
+
+    def _vote_slot(self, device: int):
+        with self._lock:
+            pool = self._vote_slots.setdefault(device, [])
+            if pool:
+                return pool.pop()
+        return kernels._SliceSlot(device)
+
+    def _release_vote_slot(self, device: int, slot) -> None:
+        with self._lock:
+            self._vote_slots.setdefault(device, []).append(slot)
+
     def vote(self, bufs: Sequence, value_type: ValueType, width: int, rel_tol, ulp_tol=None,
              voted=None, device: Optional[int] = None):
         """K-way vote on the GPU (hf_vote).  Replicas may sit on several GPUs
         (peer loads over NVLink) or in pinned host memory (UVA loads)."""
+        devs = []
+        for b in bufs:
+            if b.device.type == "cuda" and b.device.index not in devs:
+                devs.append(b.device.index)
         if device is None:
-            devs = [b.device.index for b in bufs if b.device.type == "cuda"]
             device = devs[0] if devs else 0
+        typed = value_type.numpy_dtype is not None or width in INT_DTYPES
+        if self.slice_across_gpus and len(devs) >= 2 and typed:
+            # replicas on distinct GPUs: every replica GPU votes its slice,
+            # each waiting for all replica producers (cross-device events)
+            streams = {d: self.stream(d) for d in devs}
+            for d in devs:
+                for e in devs:
+                    if e != d:
+                        streams[d].wait_stream(streams[e])
+            start = self.timer_start(streams[devs[0]], devs[0])
+            dt = torch_dtype(view_dtype(value_type, width))
+            res = kernels.vote_sliced([b.view(dt) for b in bufs], rel_tol, ulp_tol,
+                                      voted=voted.view(dt) if voted is not None else None,
+                                      devices=devs, streams=streams)
+            for d in devs[1:]:
+                streams[devs[0]].wait_stream(streams[d])
+            stop = self.timer_stop(start, streams[devs[0]], devs[0])
+            self.launches += len(devs)
+            return res, stop()
         st = self.stream(device)
-        for b in bufs:
-            if b.device.type == "cuda" and b.device.index != device:
-                st.wait_stream(self.stream(b.device.index))
-        for b in bufs:
-            if b.device.type == "cuda":
-                st.wait_stream(self.stream(b.device.index))
+        for d in devs:
+            if d != device:
+                st.wait_stream(self.stream(d))
         start = self.timer_start(st, device)
         if value_type.numpy_dtype is None and width not in INT_DTYPES:
             res = kernels.vote_bytes(list(bufs), width, voted=voted, device=device, stream=st)
@@ -259,3 +320,14 @@ class CudaBackend:
         stop = self.timer_stop(start, st, device)
         self.launches += 1
         return res, stop()
+
+
+class _PendingVote:
+    def __init__(self, backend: CudaBackend, slot, device: int, stop):
+        self._be, self._slot, self._dev, self._stop = backend, slot, device, stop
+
+    def wait(self):
+        ns = self._stop()            # synchronises the stop event (after the D2H)
+        raw = self._slot.host.numpy().tobytes()
+        self._be._release_vote_slot(self._dev, self._slot)
+        return kernels.VoteResult.from_c(_lib.HfVoteResult.from_buffer_copy(raw)), ns

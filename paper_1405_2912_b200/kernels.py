@@ -186,6 +186,65 @@ def vote_async(replicas: Sequence[torch.Tensor], ws: VoteWorkspace, rel_tol=0.00
     _count()
 
 
+class _SliceSlot:
+    """Per-device workspace + pinned host mirror for one in-flight slice."""
+
+    def __init__(self, device: int):
+        self.ws = VoteWorkspace(device)
+        self.host = torch.empty(ctypes.sizeof(HfVoteResult), dtype=torch.uint8).pin_memory()
+
+
+_SLICE_SLOTS: dict = {}
+
+
+def vote_sliced(replicas: Sequence[torch.Tensor], rel_tol=0.001, ulp_tol=None,
+                voted: Optional[torch.Tensor] = None, devices: Optional[Sequence[int]] = None,
+                streams: Optional[dict] = None):
+    """K-way vote with the element range sliced over `devices` (default: the
+    replicas' distinct GPUs): slice i runs on devices[i] and loads the other
+    replicas' slices from their GPUs over NVLink (peer access from hf_init),
+    so ingress per GPU is (K-1)/K of the unsliced voter's.  Slices launch
+    asynchronously (hf_vote_async + D2H of the 96-byte result) and combine
+    exactly on the host (sharding.combine_slices).  Returns a VoteResult."""
+    from .sharding import SliceResult, combine_slices, slice_bounds
+    K = len(replicas)
+    n = replicas[0].numel()
+    if devices is None:
+        devices = []
+        for r in replicas:
+            d = _dev(r)
+            if d not in devices:
+                devices.append(d)
+    _lib.init()
+    align = max(1, 16 // replicas[0].element_size())
+    bounds = slice_bounds(n, len(devices), align)
+    pending = []
+    for (lo, hi), d in zip(bounds, devices):
+        if hi <= lo:
+            continue
+        st = (streams or {}).get(d) or torch.cuda.current_stream(d)
+        slot = _SLICE_SLOTS.get(d)
+        if slot is None:
+            slot = _SLICE_SLOTS[d] = _SliceSlot(d)
+        views = [r[lo:hi] for r in replicas]
+        vote_async(views, slot.ws, rel_tol, ulp_tol, voted=voted[lo:hi] if voted is not None else None,
+                   stream=st)
+        copy(slot.host, slot.ws.result, stream=st)
+        ev = torch.cuda.Event()
+        ev.record(st)
+        pending.append((lo, slot, ev))
+    parts = []
+    for lo, slot, ev in pending:
+        ev.synchronize()
+        r = HfVoteResult.from_buffer_copy(slot.host.numpy().tobytes())
+        parts.append(SliceResult(lo, [int(r.mismatch[i]) for i in range(K)], int(r.unresolved), int(r.first_div)))
+    c = combine_slices(parts, K)
+    verdict_code = {"match": _lib.HF_VERDICT_MATCH, "corrected": _lib.HF_VERDICT_CORRECTED,
+                    "mismatch": _lib.HF_VERDICT_MISMATCH}[c.verdict]
+    return VoteResult(_lib.VERDICT_NAMES[verdict_code], c.mismatch, c.unresolved, c.first_div, c.winner, K,
+                      c.faulty)
+
+
 # ---- copy / checkpoint ------------------------------------------------------
 
 def _nbytes(t: torch.Tensor) -> int:

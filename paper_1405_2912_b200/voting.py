@@ -159,33 +159,44 @@ def compare(result_a: dict, result_b: dict, config: VoterConfig, backend=None) -
     return VoteOutcome("match", None, [0, 0], 0, 0)
 
 
-def vote_buffers(backend, areas: Sequence[tuple], rel_tols: Sequence[float], ulp: Optional[int] = None,
-                 device: Optional[int] = None, in_place: bool = True) -> VoteOutcome:
-    """K-way vote over device/host buffers.
+def vote_buffers_start(backend, areas: Sequence[tuple], rel_tols: Sequence[float], ulp: Optional[int] = None,
+                       device: Optional[int] = None, in_place: bool = True) -> list:
+    """Launch a K-way vote per output area without waiting.
 
-    areas: (area id, [K buffers], value type, width) in any order; they are
-    voted in sorted area order (reference rule).  With in_place the voted
-    output is written over replica 0's buffer (the kernel only stores
-    elements whose voted value differs from replica 0), so committing
-    replica 0's handles commits the voted result."""
+    areas: (area id, [K buffers], value type, width); voted in sorted area
+    order (reference rule).  With in_place the voted output is written over
+    replica 0's buffer (the kernel only stores elements whose voted value
+    differs from replica 0), so committing replica 0's handles commits the
+    voted result."""
     areas = sorted(areas, key=lambda a: a[0])
     K = len(areas[0][1]) if areas else 0
+    pending = []
+    for area, bufs, vt, width in areas:
+        if len(bufs) != K:
+            raise DispatchError(f"area {area!r}: {len(bufs)} replicas, expected {K}")
+        ulps = None if ulp is None or vt.numpy_dtype is None else [ulp] * K
+        h = backend.vote_start(bufs, vt, width, list(rel_tols), ulps,
+                               voted=bufs[0] if (in_place and K >= 3) else None, device=device)
+        pending.append((area, bufs, vt, width, h))
+    return pending
+
+
+def vote_buffers_finish(backend, pending: list) -> VoteOutcome:
+    """Wait for the votes of vote_buffers_start and combine the areas."""
+    K = len(pending[0][1]) if pending else 0
     total = [0] * K
     unresolved = 0
     first = None
     per_area = {}
     vote_ns = 0
-    for area, bufs, vt, width in areas:
-        if len(bufs) != K:
-            raise DispatchError(f"area {area!r}: {len(bufs)} replicas, expected {K}")
-        ulps = None if ulp is None or vt.numpy_dtype is None else [ulp] * K
-        res, ns = backend.vote(bufs, vt, width, list(rel_tols), ulps,
-                               voted=bufs[0] if (in_place and K >= 3) else None, device=device)
+    for area, bufs, vt, width, h in pending:
+        res, ns = h.wait()
         vote_ns += ns
         per_area[area] = res
         total = [t + m for t, m in zip(total, res.mismatch)]
         unresolved += res.unresolved
         if first is None and res.first_div >= 0:
+            # replica 0 may hold the voted value when voting in place
             raws = [backend.element_bytes(b, res.first_div, width) for b in bufs]
             vals = [_element(r, vt, width, 0) for r in raws]
             first = (area, res.first_div, vals[0], vals[1]) if K == 2 else (area, res.first_div, tuple(vals))
@@ -197,6 +208,22 @@ def vote_buffers(backend, areas: Sequence[tuple], rel_tols: Sequence[float], ulp
         verdict = "match"
     winner = min(range(K), key=lambda r: (total[r], r)) if K else 0
     return VoteOutcome(verdict, first, total, unresolved, winner, per_area, vote_ns)
+
+
+def vote_buffers(backend, areas: Sequence[tuple], rel_tols: Sequence[float], ulp: Optional[int] = None,
+                 device: Optional[int] = None, in_place: bool = True) -> VoteOutcome:
+    """Synchronous K-way vote over device/host buffers (see vote_buffers_start)."""
+    return vote_buffers_finish(backend, vote_buffers_start(backend, areas, rel_tols, ulp, device, in_place))
+
+
+class DoneVote:
+    """A vote whose result is already on the host."""
+
+    def __init__(self, res, ns):
+        self._r = (res, ns)
+
+    def wait(self):
+        return self._r
 
 
 def voter_cost_ns(config: VoterConfig, unit_kind: str, size_bytes: int) -> int:

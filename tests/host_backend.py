@@ -107,6 +107,10 @@ class HostBackend:
     def inject_bitflip(self, buf, np_dtype, idx, bit, stream=None):
         oinject.bitflip(buf.view(np_dtype), idx, bit)
 
+    def vote_start(self, bufs, value_type, width, rel_tol, ulp_tol=None, voted=None, device=None):
+        from paper_1405_2912_b200.voting import DoneVote
+        return DoneVote(*self.vote(bufs, value_type, width, rel_tol, ulp_tol, voted, device))
+
     def vote(self, bufs, value_type, width, rel_tol, ulp_tol=None, voted=None, device=None):
         from paper_1405_2912_b200.devices import INT_DTYPES, view_dtype
         t0 = time.perf_counter_ns()

@@ -316,3 +316,16 @@ def test_gemm_tc_general_signs(K):
     scale = np.abs(a).astype(np.float64) @ np.abs(b).astype(np.float64)
     err = np.abs(c.cpu().numpy() - ref)
     assert np.all(err <= 2.0 ** -9 * scale + 1e-6)
+
+
+@pytest.mark.parametrize("K", [2, 3, 5])
+def test_sliced_vote_equals_unsliced(K):
+    """Sliced multi-GPU vote path (kernels.vote_sliced), exercised on one GPU
+    with every slice on device 0: decisions and voted buffer bit-exact."""
+    from paper_1405_2912_b200 import kernels
+    rng = np.random.default_rng(K)
+    reps = _replicas(rng, K, 1_000_003, 30)
+    td = [dev(r) for r in reps]
+    voted = torch.empty_like(td[0])
+    res = kernels.vote_sliced(td, 1e-3, voted=voted, devices=[0] * K)
+    check_vote(res, ovote.vote(reps, 1e-3), voted)

@@ -158,3 +158,45 @@ def test_fault_schedule_and_decisions_match_oracle(K, strategy):
         got = rt.read_array(out)
         assert ovote.reference_first_divergence(got, data, 1e-3) is None
     assert rounds >= 25
+
+
+@pytest.mark.parametrize("depth", [1, 2])
+def test_task_stream_decisions_match_oracle(depth):
+    """Pipelined TaskStream: rounds of different tasks interleave; replaying
+    every round in its launch sequence ("seq") with the oracle must reproduce
+    each fault placement and vote decision bit-exactly."""
+    K, n = 3, 2053
+    kinds = [f"gpu-v{i}" for i in range(K)]
+    cfg = {"memory_spaces": [{"id": "host", "host": True}, {"id": "gpu0mem", "device": 0}],
+           "units": [{"id": f"u{i}", "kind": kinds[i], "memory_space": "gpu0mem", "timing": "measured",
+                      "corrupt_prob": 0.4, "corrupt_mode": "bitflip", "seed": 500 + i} for i in range(K)]}
+    rt = hf.Runtime(hf.load_fleet(cfg), hf.RuntimeConfig(serial_replicas=True, attempt_limit=200))
+    task = rt.declare_task("copy", COPY_PARAMS)
+    for i in range(K):
+        rt.attach_kernel(task, f"copy{i}", kinds[i], _copy_body)
+    rng = np.random.default_rng(1)
+    datas, reports, outs = [], [], []
+    with rt.task_stream(depth=depth) as ts:
+        for t in range(20):
+            data = rng.uniform(1, 2, n).astype(np.float32)
+            inp = rt.register_data(data.tobytes(), n, hf.ValueType.FLOAT32, "r")
+            out = rt.register_data(bytes(4 * n), n, hf.ValueType.FLOAT32, "w")
+            reports.append(ts.submit(task, {"input": inp, "output": out, "count": n}, hf.Strategy(hf.StrategyKind.HET_TMR)))
+            datas.append(data)
+            outs.append(out)
+    rounds = sorted((log["seq"], t, log) for t, r in enumerate(reports) for log in r.rounds_log)
+    rngs = {f"u{i}": random.Random(500 + i) for i in range(K)}
+    for _, t, log in rounds:
+        reps = []
+        for slot, unit in sorted(log["launched"].items()):
+            view = datas[t].copy()
+            ev = fault_schedule.apply_attempt(rngs[unit], (0, 0, 0, 0.4), [view], [True], mode="bitflip")
+            assert (log["corrupt"].get(slot) == (ev["corrupt"][1], ev["corrupt"][2])) if ev["corrupt"] \
+                else slot not in log["corrupt"]
+            reps.append(view)
+        if "verdict" in log:
+            ores = ovote.vote(reps, 1e-3)
+            assert (log["verdict"], log["mismatch"]) == (ores.verdict, ores.mismatch)
+    for t, out in enumerate(outs):
+        assert reports[t].success
+        assert ovote.reference_first_divergence(rt.read_array(out), datas[t], 1e-3) is None

@@ -451,3 +451,51 @@ def test_voter_placement_follows_cost_model():
     assert hf.place_voter(fleet, cfg, [(1_000_000, "host", "host")]).kernel == "voter_gpu"
     avoid = hf.VoterConfig(placement="avoid-task-units")
     assert hf.place_voter(fleet, avoid, [(1_000_000, "gpu1mem", "gpu2mem")], task_units=["gpu1", "gpu2"]).unit_id == "cpu0"
+
+
+# ---- pipelined task stream ------------------------------------------------------------------
+
+class TestTaskStream:
+    def _run(self, depth, over):
+        rt, task = runtime(three_units(**over), hf.RuntimeConfig(serial_replicas=True))
+        outs = []
+        with rt.task_stream(depth=depth) as ts:
+            for t in range(12):
+                data = np.full(N, t, dtype=np.float32)
+                i = rt.register_data(data.tobytes(), N, hf.ValueType.FLOAT32, "r")
+                o = rt.register_data(bytes(4 * N), N, hf.ValueType.FLOAT32, "w")
+                ts.submit(task, {"input": i, "output": o, "count": N}, DMR)
+                outs.append((o, data))
+        return rt, [rt.read_array(o) for o, _ in outs], [d + 1 for _, d in outs]
+
+    @pytest.mark.parametrize("depth", [0, 1, 3])
+    def test_stream_commits_every_task(self, depth):
+        rt, got, want = self._run(depth, {"gpu1": {"corrupt_prob": 0.4, "corrupt_rel_magnitude": 0.5}})
+        for g, w in zip(got, want):
+            assert np.array_equal(g, w)
+
+    def test_stream_respects_data_dependencies(self):
+        rt, _ = runtime(three_units())
+        task = rt.declare_task("bump", (hf.Param.area("data", "rw"), hf.Param.scalar("count")))
+
+        def bump(ctx):
+            d = ctx.request("data", "rw")
+            d[:ctx.arg("count")] += np.float32(1.0)
+
+        for k in ("cpu", "gpu"):
+            rt.attach_kernel(task, f"bump_{k}", k, bump)
+        area = rt.register_data(np.zeros(N, dtype=np.float32).tobytes(), N, hf.ValueType.FLOAT32, "rw")
+        with rt.task_stream(depth=3) as ts:
+            for _ in range(5):      # each task reads what the previous one committed
+                ts.submit(task, {"data": area, "count": N}, DMR)
+        assert np.array_equal(rt.read_array(area), np.full(N, 5.0, dtype=np.float32))
+
+    def test_rounds_log_carries_launch_order(self):
+        rt, task = runtime(three_units())
+        with rt.task_stream(depth=1) as ts:
+            reps = []
+            for t in range(4):
+                i, o, a = args_for(rt)
+                reps.append(ts.submit(task, a, DMR))
+        seqs = [log["seq"] for r in reps for log in r.rounds_log]
+        assert seqs == sorted(seqs) and len(set(seqs)) == len(seqs)
