@@ -219,13 +219,13 @@ def vote_sliced(replicas: Sequence[torch.Tensor], rel_tol=0.001, ulp_tol=None,
     align = max(1, 16 // replicas[0].element_size())
     bounds = slice_bounds(n, len(devices), align)
     pending = []
-    for (lo, hi), d in zip(bounds, devices):
+    for i, ((lo, hi), d) in enumerate(zip(bounds, devices)):
         if hi <= lo:
             continue
         st = (streams or {}).get(d) or torch.cuda.current_stream(d)
-        slot = _SLICE_SLOTS.get(d)
+        slot = _SLICE_SLOTS.get((d, i))      # one result slot per in-flight slice
         if slot is None:
-            slot = _SLICE_SLOTS[d] = _SliceSlot(d)
+            slot = _SLICE_SLOTS[(d, i)] = _SliceSlot(d)
         views = [r[lo:hi] for r in replicas]
         vote_async(views, slot.ws, rel_tol, ulp_tol, voted=voted[lo:hi] if voted is not None else None,
                    stream=st)

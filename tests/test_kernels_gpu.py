@@ -324,7 +324,7 @@ def test_sliced_vote_equals_unsliced(K):
     with every slice on device 0: decisions and voted buffer bit-exact."""
     from paper_1405_2912_b200 import kernels
     rng = np.random.default_rng(K)
-    reps = _replicas(rng, K, 1_000_003, 30)
+    reps = _replicas(rng, K, 1_000_003, np.float32, 30)
     td = [dev(r) for r in reps]
     voted = torch.empty_like(td[0])
     res = kernels.vote_sliced(td, 1e-3, voted=voted, devices=[0] * K)
