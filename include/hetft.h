@@ -63,6 +63,8 @@ extern "C" {
 /* GEMM modes for hf_gemm_tc */
 #define HF_GEMM_TF32     0   /* single-pass kind::tf32                       */
 #define HF_GEMM_3XTF32   1   /* error-compensated big+small split (3 passes) */
+#define HF_GEMM_COSCHEDULE 0x100 /* flag: launch shape that co-schedules with
+                                    concurrent kernels (2 CTAs/SM, 1 tile/CTA) */
 
 /* Result of one K-replica vote.  Plain POD; identical layout on host and
  * device (the async entry points write it in device memory). */

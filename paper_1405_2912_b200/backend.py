@@ -63,6 +63,27 @@ class CudaBackend:
                 self._streams[device] = s
         return s
 
+    def unit_stream(self, unit_id: str, device: Optional[int]):
+        """One stream per processing unit, so diverse replicas on one GPU run
+        concurrently (e.g. tcgen05 CTAs filling the SIMT kernel's last wave).
+        It first waits for the device's compute stream, where the memory
+        manager enqueued the attempt's copies, checkpoints and buffer fills."""
+        if device is None:
+            return None
+        key = ("unit", unit_id)
+        with self._lock:
+            s = self._streams.get(key)
+            if s is None:
+                s = torch.cuda.Stream(device=device)
+                self._streams[key] = s
+        s.wait_stream(self.stream(device))
+        return s
+
+    def join(self, stream, device: Optional[int]) -> None:
+        """The device's compute stream waits for `stream` (a unit stream)."""
+        if stream is not None and device is not None:
+            self.stream(device).wait_stream(stream)
+
     def copy_stream(self, device: int, direction: str = "h2d"):
         """Extra streams per device for host<->device traffic, one per
         direction (the copy engines are full duplex), so transfers overlap

@@ -34,13 +34,12 @@ constexpr int BM = 128;
 constexpr int BN = 256;
 constexpr int BK = 32;          // one 128-byte swizzle row of fp32
 constexpr int UK = 8;           // tf32 UMMA K
-constexpr int STAGES = 4;
 constexpr int A_STAGE = BM * BK * 4;   // 16 KB
 constexpr int B_STAGE = BN * BK * 4;   // 32 KB
 constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
-constexpr int TMEM_COLS = 512;
 constexpr int NUM_THREADS = 256;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+template <int S>
+constexpr int smem_bytes() { return S * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/; }
 
 // ---- PTX wrappers ----------------------------------------------------------
 
@@ -142,6 +141,7 @@ __host__ __device__ constexpr uint32_t make_idesc(int M, int N) {
            | (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
 }
 
+template <int STAGES>
 struct Barriers {
     uint64_t full[STAGES];
     uint64_t empty[STAGES];
@@ -150,6 +150,11 @@ struct Barriers {
     uint32_t tmem_base;
 };
 
+// STAGES smem ring stages; ACCS TMEM accumulators (2: persistent kernel that
+// overlaps a tile's epilogue with the next tile's main loop; 1: one tile per
+// CTA, 2 CTAs/SM co-resident, used when the kernel shares the GPU with the
+// SIMT replica so its CTAs fill the SIMT kernel's last wave).
+template <int STAGES, int ACCS>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, float* __restrict__ C,
                  int M, int N, int K) {
@@ -157,7 +162,8 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     // 1024-byte alignment for the SWIZZLE_128B atoms
     const uint32_t base_u32 = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + ((1024 - (base_u32 & 1023)) & 1023);
-    Barriers* bars = reinterpret_cast<Barriers*>(smem + STAGES * STAGE_BYTES);
+    constexpr int TMEM_COLS = ACCS * BN;
+    Barriers<STAGES>* bars = reinterpret_cast<Barriers<STAGES>*>(smem + STAGES * STAGE_BYTES);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -173,7 +179,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             mbar_init(&bars->full[s], 1);
             mbar_init(&bars->empty[s], 1);
         }
-        for (int a = 0; a < 2; ++a) {
+        for (int a = 0; a < ACCS; ++a) {
             mbar_init(&bars->tmem_full[a], 1);
             mbar_init(&bars->tmem_empty[a], 4);
         }
@@ -220,8 +226,8 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             uint32_t phase = 0;
             int local = 0;
             for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
-                const int acc = local & 1;
-                const uint32_t acc_phase = (local >> 1) & 1;
+                const int acc = local % ACCS;
+                const uint32_t acc_phase = (local / ACCS) & 1;
                 mbar_wait(&bars->tmem_empty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem + acc * BN;
@@ -255,8 +261,8 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
             const int tm = tile % tiles_m, tn = tile / tiles_m;
             const int m0 = tm * BM, n0 = tn * BN;
-            const int acc = local & 1;
-            mbar_wait(&bars->tmem_full[acc], (local >> 1) & 1);
+            const int acc = local % ACCS;
+            mbar_wait(&bars->tmem_full[acc], (local / ACCS) & 1);
             tc_fence_after();
             const int row = m0 + row_in_tile;
             const uint32_t tbase = tmem + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
@@ -400,22 +406,34 @@ static int make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t
     return HF_OK;
 }
 
+// Launch shape: persistent (4 stages, double-buffered TMEM, grid = SMs) by
+// default; co-scheduling (2 stages, 1 accumulator, grid = tiles) with
+// HF_GEMM_COSCHEDULE, when the TC replica runs concurrently with the SIMT
+// replica on the same GPU.
 // A: M x K row-major, Bt: N x K row-major (both K-major)
-static int launch(const float* A, const float* Bt, float* C, int M, int N, int K, int device, cudaStream_t st) {
+static int launch(const float* A, const float* Bt, float* C, int M, int N, int K, int device, cudaStream_t st,
+                  bool cosched) {
     CUtensorMap ta, tb;
     int rc = make_map(&ta, A, static_cast<uint64_t>(K), static_cast<uint64_t>(M), static_cast<uint64_t>(K) * 4, BK, BM);
     if (rc) return rc;
     rc = make_map(&tb, Bt, static_cast<uint64_t>(K), static_cast<uint64_t>(N), static_cast<uint64_t>(K) * 4, BK, BN);
     if (rc) return rc;
+    const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
     static bool attr_set[64] = {false};
     if (!attr_set[device]) {
-        HF_CUDA_CHECK(cudaFuncSetAttribute(gemm_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+        HF_CUDA_CHECK(cudaFuncSetAttribute(gemm_tf32_kernel<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           smem_bytes<4>()));
+        HF_CUDA_CHECK(cudaFuncSetAttribute(gemm_tf32_kernel<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           smem_bytes<2>()));
         attr_set[device] = true;
     }
-    const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-    const int sms = num_sms(device);
-    const int grid = tiles < sms ? tiles : sms;
-    gemm_tf32_kernel<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ta, tb, C, M, N, K);
+    if (cosched) {
+        gemm_tf32_kernel<2, 1><<<tiles, NUM_THREADS, smem_bytes<2>(), st>>>(ta, tb, C, M, N, K);
+    } else {
+        const int sms = num_sms(device);
+        const int grid = tiles < sms ? tiles : sms;
+        gemm_tf32_kernel<4, 2><<<grid, NUM_THREADS, smem_bytes<4>(), st>>>(ta, tb, C, M, N, K);
+    }
     HF_CHECK_LAUNCH();
     return HF_OK;
 }
@@ -427,6 +445,8 @@ extern "C" int hf_gemm_tc(const float* A, const float* B, float* C, int M, int N
                           void* stream) {
     HF_REQUIRE(A && B && C, "hf_gemm_tc: NULL operand");
     HF_REQUIRE(M > 0 && N > 0 && K > 0, "hf_gemm_tc: bad shape %dx%dx%d", M, N, K);
+    const bool cosched = (mode & HF_GEMM_COSCHEDULE) != 0;
+    mode &= ~HF_GEMM_COSCHEDULE;
     HF_REQUIRE(mode == HF_GEMM_TF32 || mode == HF_GEMM_3XTF32, "hf_gemm_tc: unknown mode %d", mode);
     if (K % 4 != 0 || N % 4 != 0 || (reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) % 16 != 0) {
         hf::set_error("hf_gemm_tc: TMA needs 16-byte aligned operands and K %% 4 == N %% 4 == 0 (got K=%d N=%d)", K, N);
@@ -462,7 +482,7 @@ extern "C" int hf_gemm_tc(const float* A, const float* B, float* C, int M, int N
                                                                  reinterpret_cast<float4*>(A3), n4);
     }
     HF_CHECK_LAUNCH();
-    int rc = hf::tc::launch(A3, Bt, C, M, N, Ke, device, st);
+    int rc = hf::tc::launch(A3, Bt, C, M, N, Ke, device, st, cosched);
     cudaFreeAsync(Bt, st);
     if (A3) cudaFreeAsync(A3, st);
     return rc;

@@ -37,16 +37,23 @@ def _mm_views(ctx):
     return a, b, c
 
 
+def _tc_flags(ctx) -> int:
+    # sharing the GPU with another replica: the co-scheduling launch shape lets
+    # tcgen05 CTAs run beside the SIMT replica's last wave
+    from ._lib import HF_GEMM_COSCHEDULE
+    return HF_GEMM_COSCHEDULE if getattr(ctx, "shared_device", False) else 0
+
+
 def mm_tc_body(ctx):
     from . import kernels
     a, b, c = _mm_views(ctx)
-    kernels.gemm_tc(a, b, c, mode=0, stream=ctx.stream)
+    kernels.gemm_tc(a, b, c, mode=0 | _tc_flags(ctx), stream=ctx.stream)
 
 
 def mm_tc3x_body(ctx):
     from . import kernels
     a, b, c = _mm_views(ctx)
-    kernels.gemm_tc(a, b, c, mode=1, stream=ctx.stream)
+    kernels.gemm_tc(a, b, c, mode=1 | _tc_flags(ctx), stream=ctx.stream)
 
 
 def mm_simt_body(ctx):
