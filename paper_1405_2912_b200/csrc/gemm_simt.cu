@@ -13,10 +13,7 @@
 // per k-tile, register double-buffered fragments, two CTAs per SM; the
 // outer product issues packed FFMA2 (fma.rn.f32x2): every output is still an
 // fp32 FMA chain in ascending k, so results equal the FFMA formulation bit
-// for bit.  A tile count that leaves a partial last wave (1024 tiles on 296
-// CTA slots at 4096^2) splits the remaining tiles along K; the last CTA of a
-// split tile adds the K-slice partials in slice order (deterministic), so
-// those outputs are two FMA chains plus one add.  Warps are laid out 4x2 over the
+// for bit.  Warps are laid out 4x2 over the
 // 16x16 thread grid so each LDS.128 of A and of B is one wavefront.
 // Generic path: 16x16 bounds-checked tiles for ragged shapes.
 #include "common.cuh"
@@ -24,14 +21,6 @@
 namespace hf {
 
 constexpr int SB_M = 128, SB_N = 128, SB_K = 16, S_STAGES = 3;
-
-// Tail split: CTAs >= full compute one K-slice of a remaining tile.
-struct SplitTail {
-    int full;          // CTAs owning whole tiles
-    int factor;        // K-slices per remaining tile (1 = no split)
-    float* work;       // remaining tiles x factor partial 128x128 tiles
-    int* counters;     // arrivals per remaining tile (zero on entry, re-armed)
-};
 
 // Packed fp32x2 FMA (sm_100 FFMA2): two independent IEEE fp32 fused
 // multiply-adds with round-to-nearest per instruction — bit-identical to two
@@ -64,7 +53,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // each other's barrier and latency stalls.
 __global__ void __launch_bounds__(256, 2)
 sgemm_128x128(const float* __restrict__ At, const float* __restrict__ B, float* __restrict__ C,
-              int M, int N, int K, SplitTail split) {
+              int M, int N, int K) {
     extern __shared__ __align__(16) float sm[];
     float* As = sm;                                   // [S][SB_K][SB_M]
     float* Bs = sm + S_STAGES * SB_K * SB_M;          // [S][SB_K][SB_N]
@@ -78,19 +67,7 @@ sgemm_128x128(const float* __restrict__ At, const float* __restrict__ B, float* 
     const int tiles_n = N / SB_N;
     const int tiles_m = M / SB_M;
     const int group = 8;
-    // CTAs [0, full) own whole tiles; the remaining tiles are split along K
-    // into `factor` CTAs each, so the last partial wave is filled
-    int bid = blockIdx.x;
-    int part = 0;
-    int k_begin = 0, k_end = K / SB_K;
-    if (bid >= split.full) {
-        const int i = bid - split.full;
-        bid = split.full + i / split.factor;
-        part = i % split.factor;
-        const int per = (K / SB_K) / split.factor;
-        k_begin = part * per;
-        k_end = k_begin + per;
-    }
+    const int bid = blockIdx.x;
     const int per_group = group * tiles_n;
     const int g = bid / per_group;
     const int first_m = g * group;
@@ -124,10 +101,10 @@ sgemm_128x128(const float* __restrict__ At, const float* __restrict__ B, float* 
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = 0ull;
 
-    const int nk = k_end - k_begin;
+    const int nk = K / SB_K;
 #pragma unroll
     for (int s = 0; s < S_STAGES - 1; ++s) {
-        if (s < nk) issue(k_begin + s, s);
+        if (s < nk) issue(s, s);
         cp_async_commit();
     }
 
@@ -136,7 +113,7 @@ sgemm_128x128(const float* __restrict__ At, const float* __restrict__ B, float* 
         __syncthreads();
         {
             const int nt = kt + S_STAGES - 1;
-            if (nt < nk) issue(k_begin + nt, nt % S_STAGES);
+            if (nt < nk) issue(nt, nt % S_STAGES);
             cp_async_commit();
         }
         const float* as = As + (kt % S_STAGES) * SB_K * SB_M;
@@ -170,40 +147,6 @@ sgemm_128x128(const float* __restrict__ At, const float* __restrict__ B, float* 
     }
     cp_async_wait<0>();
 
-    if (blockIdx.x >= split.full) {
-        // split tile: publish this K-part, the last-arriving part sums all
-        // parts in part order (deterministic regardless of arrival order)
-        const int slot = bid - split.full;
-        float* mine = split.work + (static_cast<long long>(slot) * split.factor + part) * (SB_M * SB_N);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int row = i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4);
-            *reinterpret_cast<ulonglong2*>(mine + row * SB_N + tx * 4) = make_ulonglong2(acc[i][0], acc[i][1]);
-            *reinterpret_cast<ulonglong2*>(mine + row * SB_N + 64 + tx * 4) = make_ulonglong2(acc[i][2], acc[i][3]);
-        }
-        __threadfence();
-        __syncthreads();
-        __shared__ int s_ticket;
-        if (threadIdx.x == 0) s_ticket = atomicAdd(&split.counters[slot], 1);
-        __syncthreads();
-        if (s_ticket != split.factor - 1) return;
-        __threadfence();
-        const float* base = split.work + static_cast<long long>(slot) * split.factor * (SB_M * SB_N);
-        for (int e = threadIdx.x * 4; e < SB_M * SB_N; e += blockDim.x * 4) {
-            float4 sum = __ldcg(reinterpret_cast<const float4*>(base + e));
-            for (int q = 1; q < split.factor; ++q) {
-                const float4 v = __ldcg(reinterpret_cast<const float4*>(base + static_cast<long long>(q) * SB_M * SB_N + e));
-                sum.x += v.x;
-                sum.y += v.y;
-                sum.z += v.z;
-                sum.w += v.w;
-            }
-            const int row = e / SB_N, col = e % SB_N;
-            *reinterpret_cast<float4*>(C + static_cast<long long>(m0 + row) * N + n0 + col) = sum;
-        }
-        if (threadIdx.x == 0) split.counters[slot] = 0;   // re-armed for the next launch
-        return;
-    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         const int row = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
@@ -268,29 +211,9 @@ extern "C" int hf_gemm_simt(const float* A, const float* B, float* C, int M, int
         float* At = nullptr;
         HF_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&At), static_cast<size_t>(M) * K * sizeof(float), st));
         hf::transpose_a<<<dim3(K / 32, M / 32), 256, 0, st>>>(A, At, M, K);
-        const int tiles = (M / hf::SB_M) * (N / hf::SB_N);
-        // resident CTAs: 2 per SM; split the last partial wave along K
-        const int slots = 2 * hf::num_sms(device);
-        hf::SplitTail split{tiles, 1, nullptr, nullptr};
-        const int rem = tiles % slots;
-        if (tiles > slots && rem > 0) {
-            int factor = slots / rem;
-            while (factor > 1 && (K / hf::SB_K) % factor != 0) --factor;
-            if (factor > 4) factor = 4;
-            if (factor > 1) {
-                split.full = tiles - rem;
-                split.factor = factor;
-                HF_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&split.work),
-                                              static_cast<size_t>(rem) * factor * hf::SB_M * hf::SB_N * sizeof(float), st));
-                HF_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&split.counters), rem * sizeof(int), st));
-                HF_CUDA_CHECK(cudaMemsetAsync(split.counters, 0, rem * sizeof(int), st));
-            }
-        }
-        const int grid = split.full + (tiles - split.full) * split.factor;
-        hf::sgemm_128x128<<<grid, 256, hf::SGEMM_SMEM, st>>>(At, B, C, M, N, K, split);
+        int tiles = (M / hf::SB_M) * (N / hf::SB_N);
+        hf::sgemm_128x128<<<tiles, 256, hf::SGEMM_SMEM, st>>>(At, B, C, M, N, K);
         cudaFreeAsync(At, st);
-        if (split.work) cudaFreeAsync(split.work, st);
-        if (split.counters) cudaFreeAsync(split.counters, st);
     } else {
         dim3 grid((N + 15) / 16, (M + 15) / 16);
         hf::sgemm_generic<<<grid, 256, 0, st>>>(A, B, C, M, N, K);

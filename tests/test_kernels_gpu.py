@@ -269,7 +269,7 @@ def _agree(got: np.ndarray, ref: np.ndarray, delta=1e-3):
 
 @pytest.mark.parametrize("shape", [(128, 128, 16), (256, 384, 64), (1024, 1024, 1024),
                                    (1, 1, 1), (33, 65, 17), (130, 7, 300),
-                                   (2560, 2560, 1024), (4096, 4096, 4096)])   # K-split tail paths
+                                   (2560, 2560, 1024), (4096, 4096, 4096)])
 def test_gemm_simt_within_delta(K, shape):
     M, N, Kd = shape
     rng = np.random.default_rng(M * N + Kd)
@@ -282,7 +282,7 @@ def test_gemm_simt_within_delta(K, shape):
     # of U[1,2) products stays ~1e-6 relative of the binary64 oracle
     got = c.cpu().numpy()
     _agree(got, omatmul.matmul(a, b))
-    # deterministic: a second launch (split tails included) is bit-identical
+    # deterministic: a second launch is bit-identical
     c2 = torch.empty_like(c)
     K.gemm_simt(dev(a), dev(b), c2)
     torch.cuda.synchronize()
