@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--depth", type=int, default=1, help="TaskStream depth (tasks in flight beyond the one settling)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--detect-probes", type=int, default=2000)
     ap.add_argument("--cpu-sample-s", type=float, default=12.0)
     return ap.parse_args()
 
@@ -395,6 +396,7 @@ def run_hetft_arm(args, rank, world, local):
 
     # ---- kernel-level measurements (same process, after the timed regions) ----
     kern = kernel_rooflines(device, n, kernels, torch)
+    detect = detect_rate(device, n, kernels, torch, args.seed, probes=args.detect_probes) if rank == 0 else None
 
     total_tasks = args.steps * world
     if rank != 0:
@@ -444,6 +446,7 @@ def run_hetft_arm(args, rank, world, local):
         "rooflines": kern,
         "replica_ms": {"mm_simt": simt_ns * 1e-6, "mm_tc": tc_ns * 1e-6},
         "voter_gbs_in_task": vote_gbs,
+        "detect": detect,
         "faults": {"injected": stats["injected"], "detected_mismatch_votes": stats["mismatch"],
                    "votes": stats["votes"], "rounds": stats["rounds"]},
         "cpu_baseline": cpu,
@@ -458,6 +461,54 @@ def load_peaks():
         d = json.loads(p.read_text())
         return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"]}, "MEASURED_PEAKS.json"
     return dict(PEAKS_FALLBACK), "fallback (B200_PROFILING.md)"
+
+
+def detect_rate(device, n, kernels, torch, seed: int, probes: int = 2000):
+    """Detect rate of the DMR voter on real diverse outputs: C_tc and C_simt
+    of one n x n task; each probe flips one seeded (element, bit) of C_simt,
+    votes on the GPU (hf_vote, K = 2, δ = 1e-3), flips it back.  Every GPU
+    decision is checked against the oracle predicate on that element (the
+    unflipped pair agrees everywhere, verified first).  Reports the detect
+    rate overall and per bit class and the agreement with the oracle."""
+    import random as _random
+    from oracle import vote as ovote
+    d = f"cuda:{device}"
+    g = torch.Generator(device=d)
+    g.manual_seed(seed)
+    a = torch.rand(n, n, device=d, generator=g) + 1
+    b = torch.rand(n, n, device=d, generator=g) + 1
+    c_tc = torch.empty(n, n, device=d)
+    c_si = torch.empty(n, n, device=d)
+    kernels.gemm_tc(a, b, c_tc)
+    kernels.gemm_simt(a, b, c_si)
+    x, y = c_tc.view(-1), c_si.view(-1)
+    base = kernels.vote([x, y], 1e-3)
+    if base.verdict != "match":
+        return {"error": f"unflipped TC/SIMT outputs disagree ({base.verdict}, first {base.first_div})"}
+    hx, hy = x.cpu().numpy(), y.cpu().numpy()
+    rng = _random.Random(seed * 1_000_003 + 17)
+    classes = {"0-13": [0, 0], "14": [0, 0], "15-22": [0, 0], "23-30 (exponent)": [0, 0], "31 (sign)": [0, 0]}
+    agree = detected = 0
+    for _ in range(probes):
+        e = rng.randrange(n * n)
+        bit = rng.randrange(32)
+        kernels.inject_bitflip(y, e, bit)
+        res = kernels.vote([x, y], 1e-3)
+        kernels.inject_bitflip(y, e, bit)
+        flipped = hy[e:e + 1].copy()
+        flipped.view("u4")[0] ^= 1 << bit
+        oracle_detect = not bool(ovote.pair_ok(hx[e:e + 1], flipped, 1e-3)[0])
+        gpu_detect = res.verdict == "mismatch"
+        agree += int(gpu_detect == oracle_detect and (not gpu_detect or res.first_div == e))
+        detected += int(gpu_detect)
+        key = "0-13" if bit <= 13 else "14" if bit == 14 else "15-22" if bit <= 22 else \
+            "23-30 (exponent)" if bit <= 30 else "31 (sign)"
+        classes[key][0] += int(gpu_detect)
+        classes[key][1] += 1
+    return {"probes": probes, "detect_rate": detected / probes, "oracle_agreement": agree / probes,
+            "per_bit_class": {k: (v[0] / v[1] if v[1] else None) for k, v in classes.items()},
+            "note": "one seeded bit flip per probe in the SIMT replica of a real 4096^2 TC/SIMT pair; "
+                    "known answer at δ=1e-3: bits 0-13 never, 14 ~96%, 15-31 always (uniform bit ≈ 56%)"}
 
 
 def kernel_rooflines(device, n, kernels, torch):
