@@ -1,0 +1,68 @@
+"""BASELINE config C4: voter / checkpoint bandwidth sweep on one B200.
+
+K = 2..5 fp32 replicas of 1 MB .. 4 GB each (bit-identical replicas with a
+few injected bit flips, so the common path runs), hf_vote with the voted
+output in place over replica 0, and hf_checkpoint of one buffer.  CUDA-event
+timing on the launching stream, 3 warm-up + N timed launches; replicas
+>= 64 MB exceed half the L2, smaller ones are partly L2-resident (reported
+as measured).  Writes one JSON document (default gpurun_out/sweep.json)."""
+import json
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_1405_2912_b200 import kernels  # noqa: E402
+
+
+def timed(fn, st, iters):
+    with torch.cuda.stream(st):
+        for _ in range(3):
+            fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(iters):
+            fn()
+        e1.record(st)
+    st.synchronize()
+    return e0.elapsed_time(e1) * 1e-3 / iters
+
+
+def main(out=Path("gpurun_out/sweep.json")):
+    peaks = json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").read_text()) \
+        if (Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").exists() else {"hbm_gbs": 6650.0}
+    hbm = peaks["hbm_gbs"]
+    st = torch.cuda.Stream()
+    rows = []
+    sizes = [1 << 20, 16 << 20, 64 << 20, 256 << 20, 1 << 30, 4 << 30]
+    for nbytes in sizes:
+        n = nbytes // 4
+        base = torch.rand(n, device="cuda") + 1
+        iters = 20 if nbytes <= (256 << 20) else 5
+        for K in (2, 3, 4, 5):
+            reps = [base] + [base.clone() for _ in range(K - 1)]
+            for r in range(K):
+                kernels.inject_bitflip(reps[r], (r * 7919) % n, 27)
+            ws = kernels.VoteWorkspace(0, stream=st)
+            voted = reps[0] if K >= 3 else None
+            t = timed(lambda: kernels.vote_async(reps, ws, 1e-3, voted=voted, stream=st), st, iters)
+            rd = K * nbytes
+            rows.append({"kernel": "hf_vote", "K": K, "bytes_per_replica": nbytes, "us": t * 1e6,
+                         "read_GBps": rd / t / 1e9, "frac_of_hbm": rd / t / 1e9 / hbm,
+                         "survey_GBps_(K+1)n": (K + 1) * nbytes / t / 1e9})
+            print(json.dumps(rows[-1]), flush=True)
+            del reps
+        dst = torch.empty_like(base)
+        t = timed(lambda: kernels.checkpoint(dst, base, stream=st), st, iters)
+        rows.append({"kernel": "hf_checkpoint", "bytes": nbytes, "us": t * 1e6, "GBps": 2 * nbytes / t / 1e9,
+                     "frac_of_hbm": 2 * nbytes / t / 1e9 / hbm})
+        print(json.dumps(rows[-1]), flush=True)
+        del base, dst
+        torch.cuda.empty_cache()
+    out.parent.mkdir(exist_ok=True)
+    out.write_text(json.dumps({"peak_hbm_gbs": hbm, "rows": rows}, indent=1))
+
+
+if __name__ == "__main__":
+    main(Path(sys.argv[1]) if len(sys.argv) > 1 else Path("gpurun_out/sweep.json"))
