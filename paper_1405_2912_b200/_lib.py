@@ -145,16 +145,36 @@ def check(fn: str, rc: int) -> int:
     return rc
 
 
-def init(ndev: int = 0, enable_peer_all: bool = True) -> None:
-    """hf_init once per process: device discovery and all-to-all peer access."""
+def init(ndev: int = 0, enable_peer_all: bool = False) -> None:
+    """hf_init once per process: device discovery.  Peer access is enabled
+    separately (enable_peers) so a one-GPU-per-rank process never creates
+    contexts on the other GPUs."""
     global _initialised
-    if _initialised:
+    if _initialised and not enable_peer_all:
         return
     lib = load()
     with _lock:
         if not _initialised:
-            check("hf_init", lib.hf_init(ndev, 1 if enable_peer_all else 0))
+            check("hf_init", lib.hf_init(ndev, 0))
             _initialised = True
+    if enable_peer_all:
+        enable_peers()
+
+
+_peers_enabled = False
+
+
+def enable_peers() -> None:
+    """All-to-all peer access between the visible GPUs (NVLink/NVSwitch P2P
+    for the sliced voter and peer copies/checkpoints); idempotent."""
+    global _peers_enabled
+    if _peers_enabled:
+        return
+    init()
+    with _lock:
+        if not _peers_enabled:
+            check("hf_init", load().hf_init(0, 1))
+            _peers_enabled = True
 
 
 def peer_enabled(dev: int, peer: int) -> bool:

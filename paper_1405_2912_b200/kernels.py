@@ -216,6 +216,8 @@ def vote_sliced(replicas: Sequence[torch.Tensor], rel_tol=0.001, ulp_tol=None,
             if d not in devices:
                 devices.append(d)
     _lib.init()
+    if len(set(devices)) > 1:
+        _lib.enable_peers()
     align = max(1, 16 // replicas[0].element_size())
     bounds = slice_bounds(n, len(devices), align)
     pending = []
