@@ -122,6 +122,8 @@ def vote(replicas: Sequence[torch.Tensor], rel_tol=0.001, ulp_tol=None,
     if device is None:
         device = _dev(voted) if voted is not None else _dev(replicas[0])
     _lib.init()
+    if any(r.device.type == "cuda" and r.device.index != device for r in replicas):
+        _lib.enable_peers()          # peer replicas are loaded directly over NVLink
     rel_c, ulp_c = _tolerances(K, rel_tol, ulp_tol)
     out = HfVoteResult()
     lib = _lib.load()
