@@ -200,3 +200,91 @@ def test_task_stream_decisions_match_oracle(depth):
     for t, out in enumerate(outs):
         assert reports[t].success
         assert ovote.reference_first_divergence(rt.read_array(out), datas[t], 1e-3) is None
+
+
+@pytest.mark.parametrize("seed", range(0, 300, 3))
+def test_memory_protocol_on_device_matches_model(seed):
+    """The sibling/version protocol over real HBM buffers (hf_copy,
+    hf_checkpoint, pinned host) against the flat model, as on the host
+    double in test_runtime_host.py."""
+    from oracle import memory_model
+    cfg = {"default_ns_per_byte": 0.01,
+           "memory_spaces": [{"id": "host", "host": True}, {"id": "gpu1mem", "device": 0},
+                             {"id": "gpu2mem", "device": 0}],
+           "units": [{"id": "g", "kind": "gpu", "memory_space": "gpu1mem"}]}
+    fleet = hf.load_fleet(cfg)
+    from paper_1405_2912_b200.backend import CudaBackend
+    m = hf.MemoryManager(fleet, CudaBackend())
+    ref = memory_model.SiblingModel("host")
+    rng = random.Random(seed)
+    spaces = ["host", "gpu1mem", "gpu2mem"]
+    areas = []
+    for _ in range(30):
+        op = rng.choice(["reg", "read", "read", "write", "write", "fault", "inval"])
+        if op == "reg" or not areas:
+            if len(areas) < 3:
+                size = rng.randint(1, 8) * 4
+                payload = bytes(rng.randrange(256) for _ in range(size))
+                areas.append((m.register(payload, size // 4, hf.ValueType.INT, "rw"), ref.register(payload), size))
+            continue
+        ia, ra, size = rng.choice(areas)
+        sp = rng.choice(spaces)
+        prot = rng.random() < 0.5
+        if op == "read":
+            try:
+                h = m.request(ia, sp, "r", prot)
+                got = (h.base_version, m.payload_bytes(h))
+            except hf.DataLossError:
+                got = "loss"
+            try:
+                exp = ref.read(ra, sp, prot)
+            except memory_model.ModelDataLoss:
+                exp = "loss"
+            assert got == exp
+        elif op == "write":
+            acc = rng.choice(["w", "rw"])
+            new = bytes(rng.randrange(256) for _ in range(rng.randint(0, size)))
+            try:
+                h = m.request(ia, sp, acc, prot)
+                if new:
+                    kernels.scribble(h.payload, new[:64]) if len(new) <= 64 else None
+                    new = new[:64]
+                m.commit_success([h])
+                got = h.target_version
+            except hf.DataLossError:
+                got = "loss"
+            try:
+                tok = ref.write(ra, sp, acc, prot)
+                tok[3][:len(new)] = new
+                ref.commit(tok)
+                exp = tok[2]
+            except memory_model.ModelDataLoss:
+                exp = "loss"
+            assert got == exp
+        elif op == "fault":
+            try:
+                m.request(ia, sp, "r", True)
+                m.request(ia, sp, "w", True)
+                if sp != "host":
+                    m.invalidate(ia, sp)
+                got = "ok"
+            except hf.DataLossError:
+                got = "loss"
+            try:
+                ref.read(ra, sp, True)
+                ref.write(ra, sp, "w", True)
+                ref.rollback([ra], sp)
+                exp = "ok"
+            except memory_model.ModelDataLoss:
+                exp = "loss"
+            assert got == exp
+        else:
+            if (ia, sp) in {(a, s) for a, s, _, _ in m.sibling_table()}:
+                m.invalidate(ia, sp)
+                ref.invalidate(ra, sp)
+        amap = {x: y for x, y, _ in areas}
+        assert {(amap[a], s): (v, ok) for a, s, v, ok in m.sibling_table()} == \
+            {k: (e[0], e[1]) for k, e in ref.t.items()}
+        for (a, s), (v, ok, data) in m.payload_snapshot().items():
+            if ok:
+                assert data == ref.t[(amap[a], s)][2]
