@@ -163,6 +163,13 @@ int hf_inject_scale(void* buf, int dtype, int64_t elem, double rel,
 int hf_scribble(void* buf, const uint8_t* bytes, int nbytes,
                 int device, void* stream);
 
+/* ---- test support ------------------------------------------------------- */
+/* A one-thread kernel that spins until *flag != 0 (device or mapped host
+ * memory) or for max_ns nanoseconds of %globaltimer, whichever comes first
+ * (max_ns is capped at 5 s).  It stands in for a hung replica kernel when
+ * testing the executor's stream watchdog; it can never hang the GPU. */
+int hf_debug_spin(const int* flag, int64_t max_ns, int device, void* stream);
+
 /* ---- matmul kernel variants (row-major fp32, C = A·B) -------------------- */
 /* tcgen05.mma kind::tf32 with TMA-fed, 128B-swizzled smem and TMEM
  * accumulators.  Requires M % 128 == 0, N % 128 == 0, K % 32 == 0. */

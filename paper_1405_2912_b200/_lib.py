@@ -42,6 +42,7 @@ EXPORTED = (
     "hf_vote", "hf_vote_workspace_bytes", "hf_vote_workspace_init", "hf_vote_async",
     "hf_vote_bytes", "hf_copy", "hf_fill", "hf_checkpoint", "hf_restore", "hf_checksum",
     "hf_inject_bitflip", "hf_inject_scale", "hf_scribble", "hf_gemm_tc", "hf_gemm_simt",
+    "hf_debug_spin",
 )
 
 
@@ -104,6 +105,7 @@ def _declare(lib):
         "hf_inject_bitflip": (_i32, [_c_void_p, _i32, _i64, _i32, _i32, _c_void_p]),
         "hf_inject_scale": (_i32, [_c_void_p, _i32, _i64, ctypes.c_double, _i32, _c_void_p]),
         "hf_scribble": (_i32, [_c_void_p, P(ctypes.c_uint8), _i32, _i32, _c_void_p]),
+        "hf_debug_spin": (_i32, [_c_void_p, _i64, _i32, _c_void_p]),
         "hf_gemm_tc": (_i32, [_c_void_p, _c_void_p, _c_void_p, _i32, _i32, _i32, _i32, _i32, _c_void_p]),
         "hf_gemm_simt": (_i32, [_c_void_p, _c_void_p, _c_void_p, _i32, _i32, _i32, _i32, _c_void_p]),
     }

@@ -148,7 +148,12 @@ class CudaBackend:
         def elapsed() -> int:
             ev.synchronize()
             return int(t0.elapsed_time(ev) * 1e6)
+        elapsed.start_event = t0       # the executor's watchdog polls these
+        elapsed.stop_event = ev
         return elapsed
+
+    def query(self, event) -> bool:
+        return bool(event.query())
 
     def is_device_error(self, exc: BaseException) -> bool:
         if isinstance(exc, _lib.HfError):

@@ -47,9 +47,29 @@ __global__ void scribble_kernel(uint8_t* buf, const __grid_constant__ ScribbleBy
     for (int i = threadIdx.x; i < n; i += blockDim.x) buf[i] = bytes.b[i];
 }
 
+__global__ void spin_kernel(const volatile int* flag, unsigned long long max_ns) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+        if (flag != nullptr && *flag != 0) return;
+        __nanosleep(1000);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while (t - t0 < max_ns);
+}
+
 }  // namespace hf
 
 extern "C" {
+
+int hf_debug_spin(const int* flag, int64_t max_ns, int device, void* stream) {
+    HF_REQUIRE(max_ns >= 0, "hf_debug_spin: negative duration");
+    if (max_ns > 5000000000LL) max_ns = 5000000000LL;
+    hf::DeviceGuard g(device);
+    HF_REQUIRE(g.ok, "hf_debug_spin: cannot select device %d", device);
+    hf::spin_kernel<<<1, 1, 0, hf::as_stream(stream)>>>(flag, static_cast<unsigned long long>(max_ns));
+    HF_CHECK_LAUNCH();
+    return HF_OK;
+}
 
 int hf_inject_bitflip(void* buf, int dtype, int64_t elem, int bit, int device, void* stream) {
     int w = hf::elem_size(dtype);

@@ -399,3 +399,13 @@ def gemm_tc(A: torch.Tensor, B: torch.Tensor, C: torch.Tensor, mode: int = _lib.
     check("hf_gemm_tc", _lib.load().hf_gemm_tc(A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K,
                                                mode, dev, _stream_ptr(dev, stream)))
     _count(3)           # B^T (+split) pre-pass, A round/split, tcgen05 GEMM
+
+
+def debug_spin(max_ns: int, flag: Optional[torch.Tensor] = None, device: int = 0,
+               stream: Optional[torch.cuda.Stream] = None) -> None:
+    """Launch the bounded spin kernel (a stand-in hung replica for watchdog
+    tests; capped at 5 s by the library)."""
+    _lib.init()
+    check("hf_debug_spin", _lib.load().hf_debug_spin(flag.data_ptr() if flag is not None else None,
+                                                     int(max_ns), device, _stream_ptr(device, stream)))
+    _count()

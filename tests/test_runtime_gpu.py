@@ -288,3 +288,52 @@ def test_memory_protocol_on_device_matches_model(seed):
         for (a, s), (v, ok, data) in m.payload_snapshot().items():
             if ok:
                 assert data == ref.t[(amap[a], s)][2]
+
+
+def test_watchdog_times_out_hung_replica_and_quarantines_unit():
+    """A replica whose kernel never returns within its deadline is a timeout
+    (classified while it still runs, clocked from when it started on the
+    GPU); the task re-dispatches to another unit and the hung unit is held
+    out of selection until its stream drains."""
+    import time as _time
+
+    cfg = {"memory_spaces": [{"id": "host", "host": True}, {"id": "gpu0mem", "device": 0},
+                             {"id": "gpu0ckpt", "device": 0}],
+           "units": [{"id": "ua", "kind": "gpu-a", "memory_space": "gpu0mem", "timing": "measured"},
+                     {"id": "ub", "kind": "gpu-b", "memory_space": "gpu0mem", "timing": "measured"}]}
+    rt = hf.Runtime(hf.load_fleet(cfg), hf.RuntimeConfig(default_deadline_ns=50_000_000,
+                                                         checkpoint_space="gpu0ckpt"))
+    task = rt.declare_task("copy", COPY_PARAMS)
+    calls = []
+
+    def body(ctx):
+        if not calls:
+            kernels.debug_spin(1_500_000_000, stream=ctx.stream, device=ctx.device)   # a 1.5 s hang
+        calls.append(ctx.stream)
+        _copy_body(ctx)
+
+    rt.attach_kernel(task, "ka", "gpu-a", body)
+    rt.attach_kernel(task, "kb", "gpu-b", body)
+    n = 1 << 20
+    data = np.random.default_rng(1).uniform(1, 2, n).astype(np.float32)
+    inp = rt.register_data(data.tobytes(), n, hf.ValueType.FLOAT32, "r")
+    out = rt.register_data(bytes(4 * n), n, hf.ValueType.FLOAT32, "w")
+    torch.cuda.synchronize()
+    t0 = _time.perf_counter()
+    rep = rt.invoke(task, {"input": inp, "output": out, "count": n}, hf.Strategy(hf.StrategyKind.PERF_CP))
+    got = rt.read_array(out)
+    wall = _time.perf_counter() - t0
+    assert rep.success and rep.fault_counts["timeout"] == 1 and rep.attempts == 2
+    assert np.array_equal(got, data)
+    assert wall < 1.0, f"the hang was waited out ({wall:.2f} s)"
+    hung = set(rt.executor._hung)
+    assert len(hung) == 1
+    t1 = _time.perf_counter()
+    mid = rt.invoke(task, {"input": inp, "output": out, "count": n}, hf.Strategy(hf.StrategyKind.PERF_CP))
+    assert _time.perf_counter() - t1 < 0.5 and mid.success and mid.committed.unit_id not in hung
+    assert np.array_equal(rt.read_array(out), data)
+    torch.cuda.synchronize()        # the spin ends (<= 1.5 s); the unit returns to service
+    rt.executor._reap_hung()
+    assert not rt.executor._hung
+    rep2 = rt.invoke(task, {"input": inp, "output": out, "count": n}, hf.Strategy(hf.StrategyKind.PERF_CP))
+    assert rep2.success and rep2.fault_counts["timeout"] == 0
