@@ -106,14 +106,47 @@ def _buggy_inc_body(ctx):
         dst[:n - 1].copy_(src[:n - 1]).add_(1.0)
 
 
+def _inc_oracle(data: np.ndarray) -> np.ndarray:
+    return data + np.float32(1.0)
+
+
+def _path_oracle(data: np.ndarray) -> np.ndarray:
+    left = np.concatenate((data[:1], data[:-1]))
+    right = np.concatenate((data[1:], data[-1:]))
+    return data + np.minimum(np.minimum(left, data), right)
+
+
+def _uniform_input(size: int, rng) -> np.ndarray:
+    """U[1,2) fp32 drawn element by element from `rng` (random.Random), the
+    reference's input stream (workloads.py:70-72) — experiments replay it."""
+    return np.asarray([rng.uniform(1.0, 2.0) for _ in range(size)], dtype=np.float32)
+
+
+def _vector_bind(runtime, data, size):
+    from .devices import ValueType
+    inp = runtime.register_data(data.tobytes(), size, ValueType.FLOAT32, "r")
+    out = runtime.register_data(bytes(4 * size), size, ValueType.FLOAT32, "w")
+    return {"input": inp, "output": out, "count": size}, out, [inp, out]
+
+
 @dataclass
 class Workload:
+    """A task signature plus its diverse variants (reference workloads.py:61-72).
+    ``oracle(data)`` is the expected committed output used by the experiment
+    harness to count silent corruptions; ``bind`` registers one input and
+    returns (bindings, output area, areas to release)."""
+
     name: str
     description: str
     variants: list                                   # (kernel id, unit kind, body)
+    oracle: Optional[Callable] = None
     params: tuple = field(default_factory=lambda: (Param.area("input", "r"), Param.area("output", "w"),
                                                    Param.scalar("count")))
-    make_input: Optional[Callable] = None
+    input_fn: Callable = _uniform_input
+    bind: Callable = _vector_bind
+
+    def make_input(self, size: int, rng):
+        return self.input_fn(size, rng)
 
     def attach(self, runtime, float_delta: Optional[float] = None, kinds=None):
         task = runtime.declare_task(self.name, self.params, float_delta=float_delta)
@@ -123,9 +156,28 @@ class Workload:
         return task
 
 
-def _uniform_input(size: int, rng) -> np.ndarray:
-    """U[1,2) fp32 (the reference's input distribution, workloads.py:70-72)."""
-    return np.asarray([rng.uniform(1.0, 2.0) for _ in range(size)], dtype=np.float32)
+def _matmul_input(n: int, rng):
+    """(A, B) n x n fp32 U[1,2).  numpy's PCG64 seeded from `rng`: per-element
+    Python draws are too slow at 4096^2."""
+    g = np.random.default_rng(rng.getrandbits(63))
+    a = g.random((n, n), dtype=np.float32) + np.float32(1.0)
+    b = g.random((n, n), dtype=np.float32) + np.float32(1.0)
+    return a, b
+
+
+def _matmul_oracle(data) -> np.ndarray:
+    a, b = data
+    return (a.astype(np.float64) @ b.astype(np.float64)).astype(np.float32).reshape(-1)
+
+
+def _matmul_bind(runtime, data, n):
+    from .devices import ValueType
+    a, b = data
+    vt = ValueType.FLOAT32
+    ia = runtime.register_data(a.tobytes(), n * n, vt, "r")
+    ib = runtime.register_data(b.tobytes(), n * n, vt, "r")
+    ic = runtime.register_data(bytes(4 * n * n), n * n, vt, "w")
+    return {"A": ia, "B": ib, "C": ic, "n": n}, ic, [ia, ib, ic]
 
 
 _REGISTRY: dict = {}
@@ -137,14 +189,15 @@ def _register(w: Workload) -> Workload:
 
 
 _register(Workload("inc", "increment an array of floats; identical math on every unit kind",
-                   [("inc_cpu", "cpu", _inc_body), ("inc_gpu", "gpu", _inc_body)], make_input=_uniform_input))
+                   [("inc_cpu", "cpu", _inc_body), ("inc_gpu", "gpu", _inc_body)], oracle=_inc_oracle))
 _register(Workload("pathfinder-like", "neighborhood-minimum reduction",
-                   [("path_cpu", "cpu", _path_body), ("path_gpu", "gpu", _path_body)], make_input=_uniform_input))
+                   [("path_cpu", "cpu", _path_body), ("path_gpu", "gpu", _path_body)], oracle=_path_oracle))
 _register(Workload("buggy-inc", "increment with a deterministic off-by-one bug in the GPU variant",
                    [("inc_ref_cpu", "cpu", _inc_body), ("inc_buggy_gpu", "gpu", _buggy_inc_body)],
-                   make_input=_uniform_input))
+                   oracle=_inc_oracle))
 _register(Workload("matmul", "C = A·B, fp32 n x n: tcgen05 TF32 / SIMT FP32 / tcgen05 3xTF32 variants",
-                   list(MATMUL_VARIANTS), params=MATMUL_PARAMS))
+                   list(MATMUL_VARIANTS), oracle=_matmul_oracle, params=MATMUL_PARAMS,
+                   input_fn=_matmul_input, bind=_matmul_bind))
 
 
 def builtin_workloads() -> dict:
