@@ -60,11 +60,13 @@ extern "C" {
 #define HF_VERDICT_CORRECTED  1  /* a majority exists everywhere; some replica differs */
 #define HF_VERDICT_MISMATCH   2  /* >=1 element without a majority: rerun  */
 
-/* GEMM modes for hf_gemm_tc */
+/* GEMM modes (hf_gemm_tc; hf_gemm_simt takes only the COSCHEDULE flag) */
 #define HF_GEMM_TF32     0   /* single-pass kind::tf32                       */
 #define HF_GEMM_3XTF32   1   /* error-compensated big+small split (3 passes) */
-#define HF_GEMM_COSCHEDULE 0x100 /* flag: launch shape that co-schedules with
-                                    concurrent kernels (2 CTAs/SM, 1 tile/CTA) */
+#define HF_GEMM_COSCHEDULE 0x100 /* flag: launch shapes that share SMs with a
+                                    concurrent replica of the other variant:
+                                    TC 2 stages, 1 tile/CTA; SIMT a 100 KB smem
+                                    reservation per CTA */
 
 /* Result of one K-replica vote.  Plain POD; identical layout on host and
  * device (the async entry points write it in device memory). */
@@ -175,9 +177,10 @@ int hf_debug_spin(const int* flag, int64_t max_ns, int device, void* stream);
  * accumulators.  Requires M % 128 == 0, N % 128 == 0, K % 32 == 0. */
 int hf_gemm_tc(const float* A, const float* B, float* C, int M, int N, int K,
                int mode, int device, void* stream);
-/* Register-tiled FP32 FFMA (no tensor cores). Any M, N, K >= 1. */
+/* Register-tiled FP32 FFMA (no tensor cores). Any M, N, K >= 1.
+ * mode: 0 or HF_GEMM_COSCHEDULE. */
 int hf_gemm_simt(const float* A, const float* B, float* C, int M, int N, int K,
-                 int device, void* stream);
+                 int mode, int device, void* stream);
 
 #ifdef __cplusplus
 }

@@ -107,7 +107,7 @@ def _declare(lib):
         "hf_scribble": (_i32, [_c_void_p, P(ctypes.c_uint8), _i32, _i32, _c_void_p]),
         "hf_debug_spin": (_i32, [_c_void_p, _i64, _i32, _c_void_p]),
         "hf_gemm_tc": (_i32, [_c_void_p, _c_void_p, _c_void_p, _i32, _i32, _i32, _i32, _i32, _c_void_p]),
-        "hf_gemm_simt": (_i32, [_c_void_p, _c_void_p, _c_void_p, _i32, _i32, _i32, _i32, _c_void_p]),
+        "hf_gemm_simt": (_i32, [_c_void_p, _c_void_p, _c_void_p, _i32, _i32, _i32, _i32, _i32, _c_void_p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -37,6 +37,17 @@ int num_sms(int device) {
     return sms;
 }
 
+void retain_scratch_pool(int device) {
+    static int done[64] = {0};
+    if (device < 0 || device >= 64 || __atomic_load_n(&done[device], __ATOMIC_ACQUIRE)) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    __atomic_store_n(&done[device], 1, __ATOMIC_RELEASE);
+}
+
 int elem_size(int dtype) {
     switch (dtype) {
         case HF_F32: return 4;

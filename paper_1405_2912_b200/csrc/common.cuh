@@ -16,6 +16,9 @@ void clear_error();
 
 constexpr int kNumSMs = 148;  // B200: 2 dies x 74 SMs (queried at init; this is the default)
 int num_sms(int device);
+// Keep stream-ordered scratch (cudaMallocAsync) cached in the device's
+// default pool between calls instead of returning it at every sync.
+void retain_scratch_pool(int device);
 
 // RAII device guard: switches the calling thread's current device and
 // restores it on scope exit.

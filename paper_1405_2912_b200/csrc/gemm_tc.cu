@@ -455,15 +455,7 @@ extern "C" int hf_gemm_tc(const float* A, const float* B, float* C, int M, int N
     hf::DeviceGuard g(device);
     HF_REQUIRE(g.ok, "hf_gemm_tc: cannot select device %d", device);
     cudaStream_t st = hf::as_stream(stream);
-    static bool pool_cfg[64] = {false};
-    if (!pool_cfg[device]) {  // keep stream-ordered scratch cached between calls
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-            uint64_t thr = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
-        pool_cfg[device] = true;
-    }
+    hf::retain_scratch_pool(device);
     const bool split = mode == HF_GEMM_3XTF32;
     const int Ke = split ? 3 * K : K;
     float* Bt = nullptr;

@@ -380,12 +380,13 @@ def _mm_args(A: torch.Tensor, B: torch.Tensor, C: torch.Tensor):
     return M, N, K
 
 
-def gemm_simt(A: torch.Tensor, B: torch.Tensor, C: torch.Tensor,
+def gemm_simt(A: torch.Tensor, B: torch.Tensor, C: torch.Tensor, mode: int = 0,
               stream: Optional[torch.cuda.Stream] = None) -> None:
+    """mode: 0 or HF_GEMM_COSCHEDULE (sharing the GPU with a TC replica)."""
     M, N, K = _mm_args(A, B, C)
     _lib.init()
     dev = _dev(C)
-    check("hf_gemm_simt", _lib.load().hf_gemm_simt(A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K,
+    check("hf_gemm_simt", _lib.load().hf_gemm_simt(A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K, int(mode),
                                                    dev, _stream_ptr(dev, stream)))
     fast = M % 128 == 0 and N % 128 == 0 and K % 32 == 0
     _count(2 if fast else 1)    # transpose pre-pass + sgemm

@@ -38,8 +38,8 @@ def _mm_views(ctx):
 
 
 def _tc_flags(ctx) -> int:
-    # sharing the GPU with another replica: the co-scheduling launch shape lets
-    # tcgen05 CTAs run beside the SIMT replica's last wave
+    # sharing the GPU with another replica: co-scheduling launch shapes let
+    # tcgen05 CTAs run beside SIMT CTAs on the same SMs
     from ._lib import HF_GEMM_COSCHEDULE
     return HF_GEMM_COSCHEDULE if getattr(ctx, "shared_device", False) else 0
 
@@ -59,7 +59,7 @@ def mm_tc3x_body(ctx):
 def mm_simt_body(ctx):
     from . import kernels
     a, b, c = _mm_views(ctx)
-    kernels.gemm_simt(a, b, c, stream=ctx.stream)
+    kernels.gemm_simt(a, b, c, mode=_tc_flags(ctx), stream=ctx.stream)
 
 
 MATMUL_PARAMS = (Param.area("A", "r"), Param.area("B", "r"), Param.area("C", "w"), Param.scalar("n"))

@@ -282,11 +282,18 @@ def test_gemm_simt_within_delta(K, shape):
     # of U[1,2) products stays ~1e-6 relative of the binary64 oracle
     got = c.cpu().numpy()
     _agree(got, omatmul.matmul(a, b))
-    # deterministic: a second launch is bit-identical
+    # deterministic: a second launch is bit-identical, also in the
+    # co-scheduling launch shape (same kernel, larger smem reservation)
     c2 = torch.empty_like(c)
-    K.gemm_simt(dev(a), dev(b), c2)
+    K.gemm_simt(dev(a), dev(b), c2, mode=0x100)
     torch.cuda.synchronize()
     assert c2.cpu().numpy().tobytes() == got.tobytes()
+
+
+def test_gemm_simt_rejects_unknown_mode(K):
+    x = torch.ones(128, 128, device="cuda")
+    with pytest.raises(Exception, match="unknown mode"):
+        K.gemm_simt(x, x, torch.empty_like(x), mode=1)
 
 
 @pytest.mark.parametrize("shape", [(128, 256, 32), (256, 512, 64), (1024, 1024, 1024),
