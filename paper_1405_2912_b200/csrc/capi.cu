@@ -5,6 +5,8 @@
 // access enabled all-to-all over NVLink/NVSwitch when requested.
 #include "common.cuh"
 
+#include <vector>
+
 #include <mutex>
 #include <string.h>
 
@@ -35,6 +37,46 @@ int num_sms(int device) {
         sms = kNumSMs;
     __atomic_store_n(&g_sms[device], sms, __ATOMIC_RELEASE);
     return sms;
+}
+
+static std::vector<const void*>& kernel_registry() {
+    static std::vector<const void*> v;
+    return v;
+}
+
+int register_kernels(std::initializer_list<const void*> fns) {
+    for (const void* f : fns) kernel_registry().push_back(f);
+    return 0;
+}
+
+void preload_kernels(int device) {
+    static int done[64] = {0};
+    static std::mutex mu;
+    if (device < 0 || device >= 64 || __atomic_load_n(&done[device], __ATOMIC_ACQUIRE)) return;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done[device]) return;
+    typedef int (*FuncLoad)(void*);
+    static FuncLoad func_load = nullptr;
+    static bool looked_up = false;
+    if (!looked_up) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuFuncLoad", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            func_load = reinterpret_cast<FuncLoad>(fn);
+        cudaGetLastError();
+        looked_up = true;
+    }
+    for (const void* k : kernel_registry()) {
+        cudaFuncAttributes a;
+        cudaFuncGetAttributes(&a, k);
+        if (func_load) {
+            cudaFunction_t f = nullptr;
+            if (cudaGetFuncBySymbol(&f, k) == cudaSuccess && f) func_load(f);
+        }
+    }
+    cudaGetLastError();
+    __atomic_store_n(&done[device], 1, __ATOMIC_RELEASE);
 }
 
 void retain_scratch_pool(int device) {
@@ -89,9 +131,12 @@ int hf_init(int ndev, int enable_peer_all) {
     }
     if (ndev <= 0 || ndev > count) ndev = count;
     if (ndev > 64) ndev = 64;
+    int cur = 0;
+    cudaGetDevice(&cur);
     for (int d = 0; d < ndev; ++d) {
         hf::num_sms(d);
         hf::g_peer[d][d] = 1;
+        if (d == cur) hf::preload_kernels(d);   // other devices: on first use (DeviceGuard)
     }
     if (!enable_peer_all) return HF_OK;
     int prev = 0;

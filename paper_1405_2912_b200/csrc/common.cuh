@@ -8,6 +8,8 @@
 #include <stdarg.h>
 #include "../../include/hetft.h"
 
+#include <initializer_list>
+
 namespace hf {
 
 // Thread-local last-error message (hf_last_error).
@@ -19,6 +21,13 @@ int num_sms(int device);
 // Keep stream-ordered scratch (cudaMallocAsync) cached in the device's
 // default pool between calls instead of returning it at every sync.
 void retain_scratch_pool(int device);
+// Every __global__ of the library registers itself (static initialiser) so
+// hf_init can load them all up front: with CUDA's lazy module loading the
+// first launch of a kernel may wait for the device to go idle, which would
+// stall a replica behind an unrelated long-running one (and defeat the
+// executor's watchdog).
+int register_kernels(std::initializer_list<const void*> fns);
+void preload_kernels(int device);
 
 // RAII device guard: switches the calling thread's current device and
 // restores it on scope exit.
@@ -28,6 +37,7 @@ struct DeviceGuard {
     explicit DeviceGuard(int dev) {
         if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
         if (dev >= 0 && dev != prev) ok = cudaSetDevice(dev) == cudaSuccess;
+        if (ok) preload_kernels(dev >= 0 ? dev : (prev >= 0 ? prev : 0));
     }
     ~DeviceGuard() {
         if (prev >= 0) cudaSetDevice(prev);

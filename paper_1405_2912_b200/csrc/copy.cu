@@ -183,6 +183,11 @@ static int device_of(const void* p, int* dev) {
     return HF_OK;
 }
 
+static const int kRegistered = register_kernels(
+    {(const void*)stream_kernel<true, true, true>, (const void*)stream_kernel<true, true, false>,
+     (const void*)stream_kernel<true, false, true>, (const void*)stream_kernel<true, false, false>,
+     (const void*)stream_kernel<false, true, true>, (const void*)stream_kernel<false, true, false>});
+
 }  // namespace hf
 
 extern "C" {

@@ -199,6 +199,9 @@ sgemm_generic(const float* __restrict__ A, const float* __restrict__ B, float* _
     if (row < M && col < N) C[static_cast<long long>(row) * N + col] = acc;
 }
 
+static const int kRegistered =
+    register_kernels({(const void*)sgemm_128x128, (const void*)transpose_a, (const void*)sgemm_generic});
+
 }  // namespace hf
 
 extern "C" int hf_gemm_simt(const float* A, const float* B, float* C, int M, int N, int K, int mode,

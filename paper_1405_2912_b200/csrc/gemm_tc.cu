@@ -406,6 +406,10 @@ static int make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t
     return HF_OK;
 }
 
+static const int kRegistered = register_kernels(
+    {(const void*)gemm_tf32_kernel<4, 2>, (const void*)gemm_tf32_kernel<2, 1>, (const void*)transpose_b<true>,
+     (const void*)transpose_b<false>, (const void*)round_a, (const void*)split3_a});
+
 // Launch shape: persistent (4 stages, double-buffered TMEM, grid = SMs) by
 // default; co-scheduling (2 stages, 1 accumulator, grid = tiles) with
 // HF_GEMM_COSCHEDULE, when the TC replica runs concurrently with the SIMT

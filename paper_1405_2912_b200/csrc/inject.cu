@@ -57,6 +57,9 @@ __global__ void spin_kernel(const volatile int* flag, unsigned long long max_ns)
     } while (t - t0 < max_ns);
 }
 
+static const int kRegistered = register_kernels(
+    {(const void*)bitflip_kernel, (const void*)scale_kernel, (const void*)scribble_kernel, (const void*)spin_kernel});
+
 }  // namespace hf
 
 extern "C" {

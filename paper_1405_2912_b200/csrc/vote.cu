@@ -550,6 +550,16 @@ __global__ void ws_init_kernel(VoteWorkspace* ws) {
     ws->pad = 0;
 }
 
+#define HF_VOTE_K(DT) (const void*)vote_kernel<DT, 2, 2>, (const void*)vote_kernel<DT, 3, 2>, \
+    (const void*)vote_kernel<DT, 4, 2>, (const void*)vote_kernel<DT, 5, 2>, (const void*)vote_kernel<DT, 6, 1>, \
+    (const void*)vote_kernel<DT, 7, 1>, (const void*)vote_kernel<DT, 8, 1>
+static const int kRegistered = register_kernels(
+    {HF_VOTE_K(HF_F32), HF_VOTE_K(HF_F64), HF_VOTE_K(HF_U8), HF_VOTE_K(HF_U16), HF_VOTE_K(HF_U32), HF_VOTE_K(HF_U64),
+     (const void*)vote_bytes_kernel<2>, (const void*)vote_bytes_kernel<3>, (const void*)vote_bytes_kernel<4>,
+     (const void*)vote_bytes_kernel<5>, (const void*)vote_bytes_kernel<6>, (const void*)vote_bytes_kernel<7>,
+     (const void*)vote_bytes_kernel<8>, (const void*)ws_init_kernel});
+#undef HF_VOTE_K
+
 // ---- launch ----------------------------------------------------------------
 
 using VoteKernel = void (*)(VoteParams);

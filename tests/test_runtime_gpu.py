@@ -337,3 +337,34 @@ def test_watchdog_times_out_hung_replica_and_quarantines_unit():
     assert not rt.executor._hung
     rep2 = rt.invoke(task, {"input": inp, "output": out, "count": n}, hf.Strategy(hf.StrategyKind.PERF_CP))
     assert rep2.success and rep2.fault_counts["timeout"] == 0
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4, 5, 6])
+def test_c1_tmr_1024_single_seeded_bitflip(seed):
+    """BASELINE config C1: TMR of a 1024^2 fp32 matmul (tcgen05, SIMT and
+    3xTF32 replicas) with one seeded bit flip in the tensor-core replica.
+    The fault coordinates follow the reference draw order (Appendix B, via
+    the oracle); the vote corrects it exactly when the flip moves the value
+    by more than δ — bits >= 15 always, bits <= 13 never."""
+    n = 1024
+    a, b = omatmul.make_inputs(n, seed=100 + seed)
+    rt, task = matmul_runtime(kinds=("gpu-tc", "gpu-simt", "gpu-tc3"),
+                              overrides={"gpu0.tc": {"corrupt_prob": 1.0, "corrupt_mode": "bitflip",
+                                                     "seed": seed}})
+    _, _, ic, args = register_mm(rt, a, b)
+    rep = rt.invoke(task, args, hf.Strategy(hf.StrategyKind.HET_TMR))
+    assert rep.success and len(rep.votes) == 1
+    rng = random.Random(seed)
+    assert fault_schedule.draw_class(rng, 0.0, 0.0, 0.0, 1.0) == "corrupt"
+    rng.randrange(1)
+    idx, bit = rng.randrange(n * n), rng.randrange(32)
+    log = rep.rounds_log[0]
+    slot = log["slots"].index("gpu0.tc")
+    assert rep.injected == [(slot, "gpu0.tc", idx, bit)]
+    if bit >= 15:
+        assert rep.votes == ["corrected"] and log["mismatch"][slot] == 1 and sum(log["mismatch"]) == 1
+        assert log["first_divergence"][1] == idx
+    elif bit <= 13:
+        assert rep.votes == ["match"]
+    got = rt.read_array(ic)
+    assert ovote.reference_first_divergence(got, omatmul.matmul(a, b).reshape(-1), 1e-3) is None
