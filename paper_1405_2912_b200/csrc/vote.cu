@@ -22,6 +22,9 @@
 // and a last-block epilogue that finalises the result and re-arms the
 // workspace so back-to-back votes need a single launch each.
 #include "common.cuh"
+#include <math.h>
+#include <stdlib.h>
+#include <map>
 
 #include <mutex>
 #include <vector>
@@ -50,6 +53,9 @@ struct VoteParams {
     hf_vote_result* out;
     VoteWorkspace* ws;
     int in_place;   // voted aliases replica 0: store only vectors whose voted value differs
+    // fp32 first screen (vote_elem): replica 0's magnitudes for which
+    // RN32(pdl*|x0|) is a normal number and no bound can overflow
+    float safe_lo, safe_hi;
 };
 
 template <int K>
@@ -235,6 +241,26 @@ __device__ __forceinline__ typename Elem<DT>::T vote_elem(const typename Elem<DT
                                                            const VoteParams& p, Acc<K>& acc,
                                                            unsigned long long idx) {
     using E = Elem<DT>;
+    if constexpr (DT == HF_F32) {
+        // First screen, 3 instructions per pair: with a0 = |x0| in the safe
+        // range, d = RN32(|x0-xs|) <= RN32(pdl*a0) implies d <= RN32(pdl*m)
+        // (m = max(|x0|,|xs|) >= a0, RN32 monotone) with every guard of
+        // Elem<HF_F32>::ok satisfied (its bound is normal and, since |xs| <=
+        // a0(1+pdl)(1+2^-22), cannot overflow below safe_hi), so ok() would
+        // accept the pair: same decision, no binary64.  NaN x0 fails the
+        // range test, NaN xs fails the compare; both take the full path.
+        const float f0 = __uint_as_float(x[0]);
+        const float a0 = fabsf(f0);
+        if (a0 >= p.safe_lo && a0 <= p.safe_hi) {
+            bool all = true;
+#pragma unroll
+            for (int s = 1; s < K; ++s) {
+                const int pi = pair_index<K>(0, s);
+                all &= fabsf(f0 - __uint_as_float(x[s])) <= p.pdl[pi] * a0;
+            }
+            if (__builtin_expect(all, 1)) return x[0];
+        }
+    }
     uint32_t m0 = 1u;
 #pragma unroll
     for (int s = 1; s < K; ++s) {
@@ -633,7 +659,45 @@ static int fill_params(VoteParams& p, const void* const* replicas, int K, int64_
                 p.pulp[pi] = -1;
             }
         }
+    // safe range of |x0| for the first fp32 screen (vote_elem), over replica
+    // 0's pairs; empty (lo = +inf) when any of them has the screen disabled
+    {
+        double dl_min = 1e300, dl_max = 0.0, dh_max = 0.0;
+        for (int s2 = 1; s2 < K; ++s2) {
+            const int pi = s2 - 1;   // pair_index(0, s2)
+            dl_min = dl_min < p.pdl[pi] ? dl_min : p.pdl[pi];
+            dl_max = dl_max > p.pdl[pi] ? dl_max : p.pdl[pi];
+            dh_max = dh_max > p.pdh[pi] ? dh_max : p.pdh[pi];
+        }
+        if (K < 2 || dl_min <= 0.0) {
+            p.safe_lo = INFINITY;
+            p.safe_hi = 0.0f;
+        } else {
+            const double lo = 1.1754943508222875e-38 / dl_min * (1.0 + 0x1p-20);
+            const double hi = 3.4028234663852886e38 / (dh_max * (1.0 + dl_max)) * (1.0 - 0x1p-20);
+            p.safe_lo = nextafterf(static_cast<float>(lo), INFINITY);
+            p.safe_hi = hi >= 3.4028234663852886e38 ? 3.4028234663852886e38f
+                                                    : nextafterf(static_cast<float>(hi), 0.0f);
+        }
+    }
     return HF_OK;
+}
+
+// CTAs of `k` resident per SM at 256 threads (cached per kernel and device).
+static int resident_ctas(const void* k, int device) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, int> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_pair(k, device);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, 256, 0) != cudaSuccess || nb <= 0) {
+        cudaGetLastError();
+        nb = 4;
+    }
+    cache[key] = nb;
+    return nb;
 }
 
 static int launch_vote(VoteParams& p, int K, int dtype, int width, int device, cudaStream_t st) {
@@ -642,13 +706,18 @@ static int launch_vote(VoteParams& p, int K, int dtype, int width, int device, c
     long long work = p.nvec > 0 ? p.nvec : p.n;
     long long want = (work + threads - 1) / threads;
     if (want < 1) want = 1;
-    long long cap = static_cast<long long>(sms) * 8;
-    int grid = static_cast<int>(want < cap ? want : cap);
     if (dtype >= 0) {
         VoteKernel k = select_kernel(dtype, K);
         HF_REQUIRE(k != nullptr, "hf_vote: unsupported dtype %d / K %d", dtype, K);
+        // one wave of resident CTAs striding over the buffer: no partial
+        // second wave of a memory-bound grid
+        static const int legacy = getenv("HF_VOTE_GRID_LEGACY") != nullptr;   // A/B timing only
+        long long cap = static_cast<long long>(sms) * (legacy ? 8 : resident_ctas(reinterpret_cast<const void*>(k), device));
+        int grid = static_cast<int>(want < cap ? want : cap);
         k<<<grid, threads, 0, st>>>(p);
     } else {
+        long long cap = static_cast<long long>(sms) * 8;
+        int grid = static_cast<int>(want < cap ? want : cap);
         switch (K) {
             case 2: vote_bytes_kernel<2><<<grid, threads, 0, st>>>(p, width); break;
             case 3: vote_bytes_kernel<3><<<grid, threads, 0, st>>>(p, width); break;

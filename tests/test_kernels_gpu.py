@@ -96,6 +96,37 @@ def test_k_way_vote_parity(K, Kr, dtype):
         check_vote(res, ovote.vote(reps, rel), voted)
 
 
+@pytest.mark.parametrize("Kr", [2, 3, 5])
+@pytest.mark.parametrize("rel", [1e-3, 3.7e-5, 0.25])
+def test_vote_fp32_screen_edges(K, Kr, rel):
+    """The first fp32 screen (vote_elem) accepts only inside a |x0| range
+    derived from δ: sweep |x0| across the whole binade range, around that
+    range's bounds and the exact δ boundary, with NaN/inf/±0 mixed in; every
+    decision must equal the binary64 oracle."""
+    rng = np.random.default_rng(int(rel * 1e6) + Kr)
+    d32 = np.float32(rel)
+    dl = np.float64(np.float32(d32 * np.float32(1 - 2.0 ** -18)))
+    dh = np.float64(np.float32(d32 * np.float32(1 + 2.0 ** -18)))
+    lo = np.float32(np.finfo(np.float32).tiny / dl)
+    hi = np.float32(np.finfo(np.float32).max / (dh * (1 + dl)))
+    mags = [np.float32(2.0) ** e for e in range(-149, 128, 3)]
+    for edge in (lo, hi):
+        mags += list(edge * np.float32(1) + np.arange(-8, 9, dtype=np.float32) * np.spacing(edge))
+    x0 = np.asarray(mags, dtype=np.float32)
+    x0 = np.concatenate([x0, -x0, np.float32([0.0, -0.0, np.inf, -np.inf, np.nan])])
+    n = x0.size
+    reps = [x0.copy()]
+    for r in range(1, Kr):
+        # relative offsets straddling δ: inside, at, and just outside the bound
+        f = rng.choice([0.0, 0.5, 0.999999, 1.0, 1.000001, 2.0], n) * rel * rng.choice([-1, 1], n)
+        with np.errstate(all="ignore"):
+            reps.append((x0.astype(np.float64) * (1 + f)).astype(np.float32))
+    td = [dev(r) for r in reps]
+    voted = torch.empty_like(td[0])
+    res = K.vote(td, [rel] * Kr, voted=voted)
+    check_vote(res, ovote.vote(reps, [rel] * Kr), voted)
+
+
 def test_vote_ulp_rule(K):
     rng = np.random.default_rng(5)
     for dtype in (np.float32, np.float64):

@@ -29,26 +29,29 @@ def timed(fn, st, iters):
     return e0.elapsed_time(e1) * 1e-3 / iters
 
 
-def main(out=Path("gpurun_out/sweep.json")):
+def main(out=Path("gpurun_out/sweep.json"), sizes=None, diverse=False):
     peaks = json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").read_text()) \
         if (Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").exists() else {"hbm_gbs": 6650.0}
     hbm = peaks["hbm_gbs"]
     st = torch.cuda.Stream()
     rows = []
-    sizes = [1 << 20, 16 << 20, 64 << 20, 256 << 20, 1 << 30, 4 << 30]
+    sizes = sizes or [1 << 20, 16 << 20, 64 << 20, 256 << 20, 1 << 30, 4 << 30]
     for nbytes in sizes:
         n = nbytes // 4
         base = torch.rand(n, device="cuda") + 1
         iters = 20 if nbytes <= (256 << 20) else 5
         for K in (2, 3, 4, 5):
-            reps = [base] + [base.clone() for _ in range(K - 1)]
+            # identical replicas (exact-equality path) or diverse ones (values
+            # 1e-6 apart, like TC vs SIMT outputs: the fp32 screen decides)
+            reps = [base] + [base * (1 + 1e-6 * torch.randn_like(base)) if diverse else base.clone()
+                             for _ in range(K - 1)]
             for r in range(K):
                 kernels.inject_bitflip(reps[r], (r * 7919) % n, 27)
             ws = kernels.VoteWorkspace(0, stream=st)
             voted = reps[0] if K >= 3 else None
             t = timed(lambda: kernels.vote_async(reps, ws, 1e-3, voted=voted, stream=st), st, iters)
             rd = K * nbytes
-            rows.append({"kernel": "hf_vote", "K": K, "bytes_per_replica": nbytes, "us": t * 1e6,
+            rows.append({"kernel": "hf_vote", "K": K, "diverse": diverse, "bytes_per_replica": nbytes, "us": t * 1e6,
                          "read_GBps": rd / t / 1e9, "frac_of_hbm": rd / t / 1e9 / hbm,
                          "survey_GBps_(K+1)n": (K + 1) * nbytes / t / 1e9})
             print(json.dumps(rows[-1]), flush=True)
@@ -65,4 +68,10 @@ def main(out=Path("gpurun_out/sweep.json")):
 
 
 if __name__ == "__main__":
-    main(Path(sys.argv[1]) if len(sys.argv) > 1 else Path("gpurun_out/sweep.json"))
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("out", nargs="?", default="gpurun_out/sweep.json")
+    ap.add_argument("--mib", type=int, nargs="*", help="replica sizes in MiB (default 1 MiB .. 4 GiB)")
+    ap.add_argument("--diverse", action="store_true")
+    a = ap.parse_args()
+    main(Path(a.out), [m << 20 for m in a.mib] if a.mib else None, a.diverse)
