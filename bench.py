@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--detect-probes", type=int, default=2000)
     ap.add_argument("--cpu-sample-s", type=float, default=12.0)
+    ap.add_argument("--trace-steps", action="store_true", help="per-step host wall times to stderr")
     return ap.parse_args()
 
 
@@ -338,7 +339,7 @@ def run_hetft_arm(args, rank, world, local):
     t_max = max_over_ranks(t_dev)
 
     # ---- e2e: host buffers through the same API (H2D inside invoke, D2H read) ----
-    e2e_steps = args.e2e_steps or max(3, args.steps // 2)
+    e2e_steps = args.e2e_steps or max(3, args.steps)
     hA = torch.empty(nb, dtype=torch.uint8).pin_memory()
     hB = torch.empty(nb, dtype=torch.uint8).pin_memory()
     hC = torch.empty(nb, dtype=torch.uint8).pin_memory()
@@ -367,6 +368,8 @@ def run_hetft_arm(args, rank, world, local):
                 if i + 1 < steps:
                     nxt = stage(i + 1)
                 queue.append((ts.submit(task, {"A": ia, "B": ib, "C": ic, "n": n}, strat), (ia, ib, ic)))
+                if args.trace_steps:
+                    print(f"e2e step {i} t={time.perf_counter():.6f} rounds={queue[-1][0].rounds}", file=sys.stderr)
                 while queue and queue[0][0].success:
                     rep, areas = queue.pop(0)
                     last = rt.read_into_async(areas[2], hC)

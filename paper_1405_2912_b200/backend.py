@@ -119,12 +119,18 @@ class CudaBackend:
         kernels.copy(dst, src, stream=cs)
         return self.record(cs)
 
-    def readback_copy(self, dst_host, src, src_space: MemorySpace):
+    def readback_copy(self, dst_host, src, src_space: MemorySpace, after=None):
         """Asynchronous device->host copy on the source's copy stream, ordered
-        after the compute stream's pending work; returns its event."""
+        after `after` (the event that made the payload final, e.g. its vote)
+        or, without one, after the compute stream's pending work; returns its
+        event.  Waiting on the producing event alone lets the copy of task i
+        overlap task i+1's kernels that were queued behind it."""
         dev = src_space.device
         cs = self.copy_stream(dev, "d2h")
-        cs.wait_stream(self.stream(dev))
+        if after is not None:
+            cs.wait_event(after)
+        else:
+            cs.wait_stream(self.stream(dev))
         kernels.copy(dst_host, src, stream=cs)
         return self.record(cs)
 
@@ -351,6 +357,7 @@ class CudaBackend:
 class _PendingVote:
     def __init__(self, backend: CudaBackend, slot, device: int, stop):
         self._be, self._slot, self._dev, self._stop = backend, slot, device, stop
+        self.ready = getattr(stop, "stop_event", None)   # after the vote kernel (voted bytes final)
 
     def wait(self):
         ns = self._stop()            # synchronises the stop event (after the D2H)

@@ -50,7 +50,7 @@ class HostBackend:
         dst[:] = src
         return None
 
-    def readback_copy(self, dst_host, src, src_space):
+    def readback_copy(self, dst_host, src, src_space, after=None):
         dst_host[:] = src
         return None
 
