@@ -410,7 +410,8 @@ def run_hetft_arm(args, rank, world, local):
     flops = 2.0 * n ** 3
     simt_tflops = flops / (simt_ns * 1e-9) / 1e12 if simt_ns else None
     sm_max = (clocks or {}).get("sm_max_mhz") or 1965.0
-    ffma_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12
+    ffma_peak, ffma_src = fp32_peak(sm_max)
+    traffic = ncu_traffic("sgemm_128x128", "transpose_a")
     vote_gbs = (stats["votes"] and stats["vote_ns"]) and \
         (2 * nb * sum(stats["votes"].values())) / (stats["vote_ns"] * 1e-9) / 1e9
     cpu = None
@@ -442,9 +443,10 @@ def run_hetft_arm(args, rank, world, local):
         "clocks": clocks,
         "roofline": {"bound": "fp32-simt", "kernel": "hf_gemm_simt (incl. A^T pre-pass)",
                      "achieved": simt_tflops, "peak": ffma_peak, "unit": "TFLOP/s",
-                     "frac": (simt_tflops / ffma_peak) if simt_tflops else None, "traffic": None,
-                     "peak_source": f"nominal FFMA 148 SM x 128 lanes x 2 flop x {sm_max:.0f} MHz "
-                                    "(MEASURED_PEAKS.json has no FP32 SIMT figure)",
+                     "frac": (simt_tflops / ffma_peak) if simt_tflops else None, "traffic": traffic,
+                     "traffic_unit": "DRAM bytes per launch (ncu --set full, GEMM + A^T pre-pass; "
+                                     f"operand bytes 3*{n}^2*4 = {3 * nb})",
+                     "peak_source": ffma_src,
                      "algorithmic": f"2*{n}^3 flop per launch"},
         "rooflines": kern,
         "replica_ms": {"mm_simt": simt_ns * 1e-6, "mm_tc": tc_ns * 1e-6},
@@ -456,6 +458,35 @@ def run_hetft_arm(args, rank, world, local):
         "peaks": {"source": peak_src, **peaks},
     }
     print(json.dumps(line), flush=True)
+
+
+def fp32_peak(sm_max_mhz: float):
+    """FP32 SIMT peak for the SIMT variant's roofline (MEASURED_PEAKS.json has
+    none): the packed-FFMA2 probe tools/fp32_peak (built by build()) run live
+    on this GPU, else the round's committed probe result, else nominal."""
+    exe = ROOT / "tools" / "fp32_peak"
+    if exe.exists():
+        try:
+            out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
+            d = json.loads(out.stdout.strip().splitlines()[-1])
+            if out.returncode != 0 or not d["ffma2_tflops"] > 0:
+                raise ValueError(d.get("error"))
+            return d["ffma2_tflops"], "measured live: tools/fp32_peak (FFMA2 loop, 148x4 CTAs, best of 5)"
+        except (OSError, ValueError, KeyError, IndexError, subprocess.SubprocessError):
+            pass
+    for p in sorted((ROOT / "profiles").glob("r*_fp32_peak.json"), reverse=True):
+        return json.loads(p.read_text())["ffma2_tflops"], f"measured: {p.relative_to(ROOT)} (FFMA2 probe)"
+    return 148 * 128 * 2 * sm_max_mhz * 1e6 / 1e12, f"nominal FFMA 148 SM x 128 lanes x 2 flop x {sm_max_mhz:.0f} MHz"
+
+
+def ncu_traffic(*kernels_):
+    """DRAM bytes per launch of `kernels_` summed, from the newest committed
+    ncu --set full capture summary (tools/ncu_traffic.py), or None."""
+    for p in sorted((ROOT / "profiles").glob("r*_ncu_traffic.json"), reverse=True):
+        ks = json.loads(p.read_text())["kernels"]
+        if all(k in ks for k in kernels_):
+            return sum(ks[k]["traffic_bytes"] for k in kernels_)
+    return None
 
 
 def load_peaks():
