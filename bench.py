@@ -471,7 +471,8 @@ def fp32_peak(sm_max_mhz: float):
             d = json.loads(out.stdout.strip().splitlines()[-1])
             if out.returncode != 0 or not d["ffma2_tflops"] > 0:
                 raise ValueError(d.get("error"))
-            return d["ffma2_tflops"], "measured live: tools/fp32_peak (FFMA2 loop, 148x4 CTAs, best of 5)"
+            return d["ffma2_tflops"], ("measured live: tools/fp32_peak (FFMA2 loop, 148x4 CTAs, best of 5); "
+                                       f"FFMA2 in the GEMM's broadcast operand form peaks at {d['ffma2_bcast_tflops']:.1f}")
         except (OSError, ValueError, KeyError, IndexError, subprocess.SubprocessError):
             pass
     for p in sorted((ROOT / "profiles").glob("r*_fp32_peak.json"), reverse=True):
