@@ -65,8 +65,9 @@ extern "C" {
 #define HF_GEMM_3XTF32   1   /* error-compensated big+small split (3 passes) */
 #define HF_GEMM_COSCHEDULE 0x100 /* flag: launch shapes that share SMs with a
                                     concurrent replica of the other variant:
-                                    TC 2 stages, 1 tile/CTA; SIMT a 100 KB smem
-                                    reservation per CTA */
+                                    TC 2 stages, 1 tile/CTA, operand pre-pass on
+                                    a high-priority side stream; SIMT a 100 KB
+                                    smem reservation per CTA */
 
 /* Result of one K-replica vote.  Plain POD; identical layout on host and
  * device (the async entry points write it in device memory). */

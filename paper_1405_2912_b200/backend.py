@@ -63,21 +63,29 @@ class CudaBackend:
                 self._streams[device] = s
         return s
 
-    def unit_stream(self, unit_id: str, device: Optional[int]):
+    def unit_stream(self, unit_id: str, device: Optional[int], priority: int = 0):
         """One stream per processing unit, so diverse replicas on one GPU run
         concurrently (e.g. tcgen05 CTAs filling the SIMT kernel's last wave).
         It first waits for the device's compute stream, where the memory
-        manager enqueued the attempt's copies, checkpoints and buffer fills."""
+        manager enqueued the attempt's copies, checkpoints and buffer fills.
+        priority < 0: the unit's high-priority stream (torch convention, lower
+        is higher), whose pending CTAs the GPU dispatches before those of
+        default-priority streams."""
         if device is None:
             return None
-        key = ("unit", unit_id)
+        key = ("unit", unit_id) if priority == 0 else ("unit", unit_id, priority)
         with self._lock:
             s = self._streams.get(key)
             if s is None:
-                s = torch.cuda.Stream(device=device)
+                s = torch.cuda.Stream(device=device, priority=priority)
                 self._streams[key] = s
         s.wait_stream(self.stream(device))
         return s
+
+    def follow(self, stream, device: Optional[int]) -> None:
+        """`stream` waits for the device's compute stream (no host blocking)."""
+        if stream is not None and device is not None:
+            stream.wait_stream(self.stream(device))
 
     def join(self, stream, device: Optional[int]) -> None:
         """The device's compute stream waits for `stream` (a unit stream)."""
@@ -180,6 +188,15 @@ class CudaBackend:
             kernels.fill(buf, 0, stream=self.stream(space.device))
         return buf
 
+    def reserve(self, space: MemorySpace, nbytes: int, count: int) -> None:
+        """Grow the caching allocator to hold `count` free `nbytes` blocks on
+        the space's compute stream (host spaces: nothing to do)."""
+        if space.device is None or nbytes <= 0 or count <= 0:
+            return
+        with torch.cuda.stream(self.stream(space.device)):
+            bufs = [torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{space.device}") for _ in range(count)]
+        del bufs
+
     def from_bytes(self, space: MemorySpace, data) -> torch.Tensor:
         raw = np.frombuffer(bytes(data), dtype=np.uint8)
         buf = self.alloc(space, raw.size, zero=False)
@@ -200,12 +217,25 @@ class CudaBackend:
     def nbytes(self, buf) -> int:
         return int(buf.numel())
 
-    def element_bytes(self, buf, idx: int, width: int) -> bytes:
+    def element_bytes(self, buf, idx: int, width: int, after=None) -> bytes:
+        """Raw bytes of one element.  With `after` (the event that made the
+        buffer final, e.g. its vote) only that event is awaited, on a side
+        stream: draining the whole compute stream would also wait for the
+        next task's kernels queued behind the vote, which delayed every
+        re-dispatch of a mismatching vote by one full task."""
         part = buf[idx * width:(idx + 1) * width]
-        if part.device.type == "cuda":
-            self.synchronize(self.stream(part.device.index))
+        if part.device.type != "cuda":
+            return part.numpy().tobytes()
+        dev = part.device.index
+        if after is None:
+            self.synchronize(self.stream(dev))
             return part.cpu().numpy().tobytes()
-        return part.numpy().tobytes()
+        cs = self.copy_stream(dev, "peek")
+        cs.wait_event(after)
+        host = torch.empty(width, dtype=torch.uint8, pin_memory=True)
+        kernels.copy(host, part, stream=cs)
+        cs.synchronize()
+        return host.numpy().tobytes()
 
     def copy(self, dst, dst_space: MemorySpace, src, src_space: MemorySpace) -> None:
         """dst <- src on the destination's stream (or the source's when the

@@ -79,6 +79,62 @@ void preload_kernels(int device) {
     __atomic_store_n(&done[device], 1, __ATOMIC_RELEASE);
 }
 
+cudaError_t SideStream::fork(cudaStream_t st) {
+    cudaError_t e = cudaEventRecord(fork_ev, st);
+    return e != cudaSuccess ? e : cudaStreamWaitEvent(stream, fork_ev, 0);
+}
+
+cudaError_t SideStream::join(cudaStream_t st) {
+    cudaError_t e = cudaEventRecord(join_ev, stream);
+    return e != cudaSuccess ? e : cudaStreamWaitEvent(st, join_ev, 0);
+}
+
+void SideStream::lock() { static_cast<std::mutex*>(mu)->lock(); }
+void SideStream::unlock() { static_cast<std::mutex*>(mu)->unlock(); }
+
+SideStream* side_stream(int device, int level) {
+    constexpr int kLevels = 2;
+    static SideStream sides[64][kLevels];
+    static std::mutex mus[64][kLevels];
+    static std::once_flag once[64][kLevels];
+    if (device < 0 || device >= 64 || level < 0 || level >= kLevels) return nullptr;
+    SideStream* s = &sides[device][level];
+    std::call_once(once[device][level], [s, device, level] {
+        int least = 0, greatest = 0;
+        if (cudaDeviceGetStreamPriorityRange(&least, &greatest) != cudaSuccess) return;
+        int prio = greatest + level;     // greatest is the most negative
+        if (prio > least) prio = least;
+        s->mu = &mus[device][level];
+        if (cudaStreamCreateWithPriority(&s->stream, cudaStreamNonBlocking, prio) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s->fork_ev, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s->join_ev, cudaEventDisableTiming) != cudaSuccess)
+            s->stream = nullptr;
+    });
+    return s->stream ? s : nullptr;
+}
+
+cudaError_t begin_side_launch(SideStream* side, cudaStream_t st, cudaStream_t* launch_stream) {
+    *launch_stream = st;
+    if (!side) return cudaSuccess;
+    side->lock();
+    cudaError_t e = side->fork(st);
+    if (e != cudaSuccess) {
+        side->unlock();
+        return e;
+    }
+    *launch_stream = side->stream;
+    return cudaSuccess;
+}
+
+cudaError_t end_side_launch(SideStream* side, cudaStream_t st) {
+    cudaError_t e = cudaGetLastError();
+    if (side) {
+        if (e == cudaSuccess) e = side->join(st);
+        side->unlock();
+    }
+    return e;
+}
+
 void retain_scratch_pool(int device) {
     static int done[64] = {0};
     if (device < 0 || device >= 64 || __atomic_load_n(&done[device], __ATOMIC_ACQUIRE)) return;

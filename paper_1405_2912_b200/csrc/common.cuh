@@ -21,6 +21,28 @@ int num_sms(int device);
 // Keep stream-ordered scratch (cudaMallocAsync) cached in the device's
 // default pool between calls instead of returning it at every sync.
 void retain_scratch_pool(int device);
+// High-priority side streams for the operand pre-passes of co-scheduled
+// GEMM replicas (HF_GEMM_COSCHEDULE).  level 0 = the device's greatest
+// stream priority, level 1 = the next one down.  fork() makes the side
+// stream wait for `st`'s pending work; join() makes `st` wait for what was
+// launched on the side stream.  The caller holds `mu` between the two so
+// concurrent callers cannot interleave their event record/wait pairs.
+struct SideStream {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+    void* mu = nullptr;   // std::mutex (kept out of this header)
+    cudaError_t fork(cudaStream_t st);
+    cudaError_t join(cudaStream_t st);
+    void lock();
+    void unlock();
+};
+SideStream* side_stream(int device, int level);
+// begin: lock + fork, *launch_stream = side stream (or `st` when side is
+// NULL).  end: check the launches, join back into `st`, unlock.  Both return
+// the first CUDA error; end always unlocks.
+cudaError_t begin_side_launch(SideStream* side, cudaStream_t st, cudaStream_t* launch_stream);
+cudaError_t end_side_launch(SideStream* side, cudaStream_t st);
+
 // Every __global__ of the library registers itself (static initialiser) so
 // hf_init can load them all up front: with CUDA's lazy module loading the
 // first launch of a kernel may wait for the device to go idle, which would

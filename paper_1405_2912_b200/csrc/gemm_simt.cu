@@ -224,7 +224,16 @@ extern "C" int hf_gemm_simt(const float* A, const float* B, float* C, int M, int
         }
         float* At = nullptr;
         HF_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&At), static_cast<size_t>(M) * K * sizeof(float), st));
-        hf::transpose_a<<<dim3(K / 32, M / 32), 256, 0, st>>>(A, At, M, K);
+        // Co-scheduled: the A^T pre-pass runs on the device's greatest-priority
+        // side stream, ahead of the tensor-core replica's pre-pass (level 1),
+        // so this GEMM's grid is pending before the TC GEMM's and, launched on
+        // the executor's higher-priority lead stream, is dispatched first; the
+        // TC CTAs then fill its last wave.
+        hf::SideStream* side = (mode & HF_GEMM_COSCHEDULE) ? hf::side_stream(device, 0) : nullptr;
+        cudaStream_t ps = st;
+        HF_CUDA_CHECK(hf::begin_side_launch(side, st, &ps));
+        hf::transpose_a<<<dim3(K / 32, M / 32), 256, 0, ps>>>(A, At, M, K);
+        HF_CUDA_CHECK(hf::end_side_launch(side, st));
         int tiles = (M / hf::SB_M) * (N / hf::SB_N);
         const int smem = (mode & HF_GEMM_COSCHEDULE) ? hf::SGEMM_SMEM_COSCHED : hf::SGEMM_SMEM;
         hf::sgemm_128x128<<<tiles, 256, smem, st>>>(At, B, C, M, N, K);

@@ -465,19 +465,27 @@ extern "C" int hf_gemm_tc(const float* A, const float* B, float* C, int M, int N
     float* Bt = nullptr;
     float* A3 = nullptr;
     HF_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&Bt), static_cast<size_t>(N) * Ke * sizeof(float), st));
+    HF_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&A3), static_cast<size_t>(M) * Ke * sizeof(float), st));
+    // Co-scheduled with a SIMT replica: the pre-pass runs on a high-priority
+    // side stream (level 1: one below the SIMT pre-pass), so its CTAs are
+    // dispatched ahead of the SIMT GEMM's pending CTAs, while the GEMM itself
+    // stays on the caller's (lower-priority) stream and fills the SIMT grid's
+    // last wave.  Without it the pre-pass, and so the GEMM, waited for that
+    // last wave whenever the SIMT grid reached the GPU first.
+    hf::SideStream* side = cosched ? hf::side_stream(device, 1) : nullptr;
+    cudaStream_t ps = st;
+    HF_CUDA_CHECK(hf::begin_side_launch(side, st, &ps));
     dim3 tgrid((N + 31) / 32, (K + 31) / 32);
     if (split) {
-        hf::tc::transpose_b<true><<<tgrid, 256, 0, st>>>(B, Bt, K, N);
-        HF_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&A3), static_cast<size_t>(M) * Ke * sizeof(float), st));
-        hf::tc::split3_a<<<hf::num_sms(device) * 8, 256, 0, st>>>(A, A3, M, K);
+        hf::tc::transpose_b<true><<<tgrid, 256, 0, ps>>>(B, Bt, K, N);
+        hf::tc::split3_a<<<hf::num_sms(device) * 8, 256, 0, ps>>>(A, A3, M, K);
     } else {
-        hf::tc::transpose_b<false><<<tgrid, 256, 0, st>>>(B, Bt, K, N);
-        HF_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&A3), static_cast<size_t>(M) * K * sizeof(float), st));
+        hf::tc::transpose_b<false><<<tgrid, 256, 0, ps>>>(B, Bt, K, N);
         const long long n4 = static_cast<long long>(M) * K / 4;  // K % 4 == 0
-        hf::tc::round_a<<<hf::num_sms(device) * 8, 256, 0, st>>>(reinterpret_cast<const float4*>(A),
+        hf::tc::round_a<<<hf::num_sms(device) * 8, 256, 0, ps>>>(reinterpret_cast<const float4*>(A),
                                                                  reinterpret_cast<float4*>(A3), n4);
     }
-    HF_CHECK_LAUNCH();
+    HF_CUDA_CHECK(hf::end_side_launch(side, st));
     int rc = hf::tc::launch(A3, Bt, C, M, N, Ke, device, st, cosched);
     cudaFreeAsync(Bt, st);
     if (A3) cudaFreeAsync(A3, st);

@@ -197,7 +197,9 @@ def vote_buffers_finish(backend, pending: list) -> VoteOutcome:
         unresolved += res.unresolved
         if first is None and res.first_div >= 0:
             # replica 0 may hold the voted value when voting in place
-            raws = [backend.element_bytes(b, res.first_div, width) for b in bufs]
+            after = getattr(h, "ready", None)
+            raws = [backend.element_bytes(b, res.first_div, width, after=after) if after is not None
+                    else backend.element_bytes(b, res.first_div, width) for b in bufs]
             vals = [_element(r, vt, width, 0) for r in raws]
             first = (area, res.first_div, vals[0], vals[1]) if K == 2 else (area, res.first_div, tuple(vals))
     if unresolved:

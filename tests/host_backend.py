@@ -79,7 +79,7 @@ class HostBackend:
     def nbytes(self, buf):
         return int(buf.size)
 
-    def element_bytes(self, buf, idx, width):
+    def element_bytes(self, buf, idx, width, after=None):
         return buf[idx * width:(idx + 1) * width].tobytes()
 
     def copy(self, dst, dst_space, src, src_space):
