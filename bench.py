@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None, help="default max(40, --steps)")
     ap.add_argument("--depth", type=int, default=1, help="TaskStream depth (tasks in flight beyond the one settling)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-tmr", action="store_true", help="skip the HetTMR 4096^2 side measurement")
     ap.add_argument("--detect-probes", type=int, default=2000)
     ap.add_argument("--cpu-sample-s", type=float, default=12.0)
     ap.add_argument("--trace-steps", action="store_true", help="per-step host wall times to stderr")
@@ -408,6 +409,8 @@ def run_hetft_arm(args, rank, world, local):
 
     # ---- kernel-level measurements (same process, after the timed regions) ----
     kern = kernel_rooflines(device, n, kernels, torch)
+    tmr = tmr_rate(device, n, args.fault_prob, args.seed + 7919 * rank, args.steps, args.warmup, torch) \
+        if not args.no_tmr else None
     detect = detect_rate(device, n, kernels, torch, args.seed, probes=args.detect_probes) if rank == 0 else None
 
     total_tasks = args.steps * world
@@ -461,6 +464,7 @@ def run_hetft_arm(args, rank, world, local):
         "rooflines": kern,
         "replica_ms": {"mm_simt": simt_ns * 1e-6, "mm_tc": tc_ns * 1e-6},
         "voter_gbs_in_task": vote_gbs,
+        "tmr": tmr,
         "detect": detect,
         "faults": {"injected": stats["injected"], "detected_mismatch_votes": stats["mismatch"],
                    "votes": stats["votes"], "rounds": stats["rounds"]},
@@ -606,6 +610,71 @@ def kernel_rooflines(device, n, kernels, torch):
     out["hf_gemm_simt"] = {"bound": "fp32-simt", "achieved": 2 * n ** 3 / t / 1e12, "unit": "TFLOP/s",
                            "us": t * 1e6}
     return out
+
+
+def tmr_rate(device, n, fault_prob, seed, steps, warmup, torch):
+    """North-star headline shape on one GPU: HetTMR of the three diverse
+    variants (tcgen05 TF32, SIMT FP32, tcgen05 3xTF32) on a 4096^2 fp32
+    matmul, device-resident inputs checkpointed into HBM, bit-flip faults at
+    the same per-replica probability, majority vote (K = 3) corrects a single
+    faulty replica.  CUDA-event timed on the runtime's compute stream."""
+    import paper_1405_2912_b200 as hf
+    kinds = ("gpu-tc", "gpu-simt", "gpu-tc3")
+    cfg = hf.gpu_fleet_config(devices=(device,), kinds=kinds)
+    cfg["memory_spaces"].append({"id": f"gpu{device}ckpt", "device": device, "label": "HBM checkpoint reserve"})
+    for i, u in enumerate(cfg["units"]):
+        u.update({"corrupt_prob": fault_prob, "corrupt_mode": "bitflip", "seed": seed * 1_000_003 + i * 101 + 31})
+    rt = hf.Runtime(hf.load_fleet(cfg), hf.RuntimeConfig(checkpoint_space=f"gpu{device}ckpt",
+                                                         serial_replicas=True, attempt_limit=64))
+    task = hf.get_workload("matmul").attach(rt, kinds=kinds)
+    space = f"gpu{device}mem"
+    nb = n * n * 4
+    rt.reserve(space, nb, 24)
+    g = torch.Generator(device=f"cuda:{device}")
+    g.manual_seed(seed * 7919 + 5)
+    A = (torch.rand(n * n, device=f"cuda:{device}", generator=g) + 1).view(torch.uint8)
+    B = (torch.rand(n * n, device=f"cuda:{device}", generator=g) + 1).view(torch.uint8)
+    C0 = torch.zeros(nb, dtype=torch.uint8, device=f"cuda:{device}")
+    strat = hf.Strategy(hf.StrategyKind.HET_TMR)
+    votes, rounds = {}, 0
+
+    def go(k, recording):
+        nonlocal rounds
+        queue = []
+        with rt.task_stream(depth=1) as ts:
+            for _ in range(k):
+                areas = tuple(rt.register_device_data(x, n * n, hf.ValueType.FLOAT32, m, space)
+                              for x, m in ((A, "r"), (B, "r"), (C0, "w")))
+                queue.append((ts.submit(task, dict(zip("ABC", areas), n=n), strat), areas))
+                while queue and queue[0][0].success:
+                    rep, ar = queue.pop(0)
+                    if recording:
+                        rounds += rep.rounds
+                        for v in rep.votes:
+                            votes[v] = votes.get(v, 0) + 1
+                    for x in ar:
+                        rt.release(x)
+        for rep, ar in queue:
+            if recording:
+                rounds += rep.rounds
+                for v in rep.votes:
+                    votes[v] = votes.get(v, 0) + 1
+            for x in ar:
+                rt.release(x)
+
+    go(max(3, warmup), False)
+    st = rt.backend.stream(device)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    go(steps, True)
+    e1.record(st)
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) * 1e-3
+    return {"value": steps / t, "unit": "tasks/s", "ms_per_task": 1e3 * t / steps, "steps": steps,
+            "workload": f"HetTMR {n}x{n} fp32 matmul (tcgen05 TF32 + SIMT FP32 + tcgen05 3xTF32 replicas "
+                        f"on 1 GPU), HBM checkpoint of inputs, bit flips p={fault_prob}/replica, K=3 majority vote",
+            "votes": votes, "rounds": rounds}
 
 
 def main():

@@ -26,6 +26,7 @@
 
 #include <cuda.h>
 #include <mutex>
+#include <stdlib.h>
 
 namespace hf {
 namespace tc {
@@ -298,6 +299,314 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     }
 }
 
+// ---- CTA-pair variant (cta_group::2) ---------------------------------------
+// A cluster of two CTAs on one TPC computes a 256 x 256 tile with
+// tcgen05.mma.cta_group::2 (M = 256): CTA rank r stages rows [128r, 128r+128)
+// of the A tile and rows [128r, 128r+128) of the B^T tile, the tensor cores of
+// the pair read both halves, and each CTA's TMEM accumulates its 128 rows x
+// 256 columns.  Per 256 x 256 x 32 k-block the pair moves 64 KB through L2
+// instead of the 96 KB two single-CTA 128 x 256 tiles need, and each SM's
+// shared memory takes 32 KB of TMA writes instead of 48 KB.
+//   leader (rank 0): warp 0 TMA (its halves; arms the stage's full barrier
+//                    with both CTAs' bytes), warp 1 MMA issue, warp 2 TMEM
+//   peer   (rank 1): warp 0 TMA (its halves, completing on the leader's
+//                    barrier), warp 2 TMEM
+//   both: warps 4..7 epilogue of their own 128 rows; commits multicast to
+//         both CTAs' barriers; the leader's tmem_empty counts 8 warps.
+constexpr int PBM = 256;            // pair tile rows (128 per CTA)
+constexpr int PBN = 256;            // pair tile cols (B^T rows, 128 per CTA)
+constexpr int P_STAGE = (PBM / 2) * BK * 4 + (PBN / 2) * BK * 4;   // 32 KB per CTA
+template <int S>
+constexpr int pair_smem_bytes() { return S * P_STAGE + 1024 + 256; }
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+// shared::cluster address of the same smem offset in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t map_rank(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
+                                                 int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+        "[%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tc_mma_tf32_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+
+// Tail split (stream-K style, deterministic): of T pair tiles over P pairs,
+// the last R = T mod P tiles are cut into `splits` k-ranges so the final
+// round keeps R*splits <= P pairs busy instead of R.  Split j < splits-1
+// stores its 128 x 256 partial per CTA into `partial` and raises its flag;
+// the last split waits for the flags and writes C = ((P0 + P1) + ...) + own,
+// a fixed summation order, so results are run-to-run identical.
+struct PairSplit {
+    int full_tiles;      // T - R tiles computed whole
+    int splits;          // k-ranges per tail tile (1: no split)
+    float* partial;      // R * (splits-1) slots of 256 x 256 floats
+    int* flags;          // R * (splits-1) * 2 (per CTA rank), zeroed per launch
+};
+
+__device__ __forceinline__ void store_release_gpu(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ int load_acquire_gpu(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <int STAGES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      float* __restrict__ C, int M, int N, int K, PairSplit sp) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t base_u32 = smem_u32(smem_raw);
+    uint8_t* smem = smem_raw + ((1024 - (base_u32 & 1023)) & 1023);
+    constexpr int ACCS = 2;
+    constexpr int TMEM_COLS = ACCS * PBN;
+    constexpr int A_HALF = (PBM / 2) * BK * 4;   // 16 KB
+    Barriers<STAGES>* bars = reinterpret_cast<Barriers<STAGES>*>(smem + STAGES * P_STAGE);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const int pair = blockIdx.x >> 1;
+    const int npairs = gridDim.x >> 1;
+    const int tiles_m = (M + PBM - 1) / PBM;
+    const int tiles_n = (N + PBN - 1) / PBN;
+    const int num_tiles = tiles_m * tiles_n;
+    const int nkb = (K + BK - 1) / BK;
+    const int tail = num_tiles - sp.full_tiles;
+    const int num_units = sp.full_tiles + tail * sp.splits;
+    // unit -> (tile, k-block range, split index)
+    auto unit_of = [&](int u, int& tile, int& kb0, int& kb1, int& split) {
+        if (u < sp.full_tiles) {
+            tile = u, kb0 = 0, kb1 = nkb, split = -1;
+        } else {
+            const int v = u - sp.full_tiles;
+            tile = sp.full_tiles + v / sp.splits;
+            split = v % sp.splits;
+            kb0 = static_cast<int>(static_cast<long long>(nkb) * split / sp.splits);
+            kb1 = static_cast<int>(static_cast<long long>(nkb) * (split + 1) / sp.splits);
+        }
+    };
+
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tmA);
+        prefetch_tmap(&tmB);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&bars->full[s], 1);
+            mbar_init(&bars->empty[s], 1);
+        }
+        for (int a = 0; a < ACCS; ++a) {
+            mbar_init(&bars->tmem_full[a], 1);
+            mbar_init(&bars->tmem_empty[a], 8);     // 4 epilogue warps x 2 CTAs (leader's copy is used)
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&bars->tmem_base)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    cluster_sync_all();      // both CTAs' barriers initialised and TMEM allocated
+    tc_fence_after();
+    const uint32_t tmem = bars->tmem_base;
+
+    if (warp == 0) {
+        // ===== TMA producer (both CTAs): this CTA's A and B^T halves =====
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int u = pair; u < num_units; u += npairs) {
+                int tile, kb0, kb1, split;
+                unit_of(u, tile, kb0, kb1, split);
+                const int tm = tile % tiles_m, tn = tile / tiles_m;
+                const int m0 = tm * PBM + static_cast<int>(rank) * (PBM / 2);
+                const int n0 = tn * PBN + static_cast<int>(rank) * (PBN / 2);
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    mbar_wait(&bars->empty[stage], phase ^ 1);
+                    const uint32_t sa = smem_u32(smem + stage * P_STAGE);
+                    const uint32_t sb = sa + A_HALF;
+                    const uint32_t full_leader = map_rank(smem_u32(&bars->full[stage]), 0);
+                    if (rank == 0) mbar_expect_tx(&bars->full[stage], 2 * P_STAGE);
+                    tma_load_2d_pair(sa, &tmA, full_leader, kb * BK, m0);
+                    tma_load_2d_pair(sb, &tmB, full_leader, kb * BK, n0);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer (leader only) =====
+        if (rank == 0 && lane == 0) {
+            constexpr uint32_t idesc = make_idesc(PBM, PBN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int local = 0;
+            for (int u = pair; u < num_units; u += npairs, ++local) {
+                int tile, kb0, kb1, split;
+                unit_of(u, tile, kb0, kb1, split);
+                const int acc = local % ACCS;
+                const uint32_t acc_phase = (local / ACCS) & 1;
+                mbar_wait(&bars->tmem_empty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem + acc * PBN;
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    mbar_wait(&bars->full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(smem + stage * P_STAGE);
+                    const uint32_t sb = sa + A_HALF;
+#pragma unroll
+                    for (int kk = 0; kk < BK / UK; ++kk) {
+                        uint64_t adesc = make_desc(sa + kk * UK * 4, 16, 1024);
+                        uint64_t bdesc = make_desc(sb + kk * UK * 4, 16, 1024);
+                        tc_mma_tf32_pair(d_tmem, adesc, bdesc, idesc, (kb != kb0) | kk);
+                    }
+                    tc_commit_pair(&bars->empty[stage]);      // frees the stage in both CTAs
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                tc_commit_pair(&bars->tmem_full[acc]);        // both CTAs' epilogues
+            }
+        }
+    } else if (warp >= 4) {
+        // ===== epilogue (both CTAs): own 128 rows x 256 cols =====
+        const int ew = warp - 4;
+        const int row_in_tile = static_cast<int>(rank) * (PBM / 2) + ew * 32 + lane;
+        const uint32_t empty_leader_base = map_rank(smem_u32(&bars->tmem_empty[0]), 0);
+        const int etid = threadIdx.x - 128;          // 0..127 over the 4 epilogue warps
+        int local = 0;
+        for (int u = pair; u < num_units; u += npairs, ++local) {
+            int tile, kb0, kb1, split;
+            unit_of(u, tile, kb0, kb1, split);
+            const int tm = tile % tiles_m, tn = tile / tiles_m;
+            const int m0 = tm * PBM, n0 = tn * PBN;
+            const int acc = local % ACCS;
+            mbar_wait(&bars->tmem_full[acc], (local / ACCS) & 1);
+            tc_fence_after();
+            const int row = m0 + row_in_tile;
+            const uint32_t tbase = tmem + (static_cast<uint32_t>(ew * 32) << 16) + acc * PBN;
+            float* crow = C + static_cast<long long>(row) * N;
+            // tail-split bookkeeping: this CTA's 128 x 256 slot of tail tile t
+            const int t = tile - sp.full_tiles;
+            const bool partial_out = split >= 0 && split < sp.splits - 1;
+            const bool fixup = split == sp.splits - 1 && sp.splits > 1;
+            auto slot = [&](int j) {
+                return sp.partial + ((static_cast<long long>(t) * (sp.splits - 1) + j) * PBM +
+                                     static_cast<int>(rank) * (PBM / 2) + ew * 32 + lane) * PBN;
+            };
+            auto flag = [&](int j) { return sp.flags + (t * (sp.splits - 1) + j) * 2 + static_cast<int>(rank); };
+            if (fixup) {      // earlier k-ranges of this tile must have landed
+                if (etid == 0)
+                    for (int j = 0; j < sp.splits - 1; ++j)
+                        while (load_acquire_gpu(flag(j)) == 0) __nanosleep(64);
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+            }
+#pragma unroll 1
+            for (int c = 0; c < PBN / 32; ++c) {
+                float v[32];
+                tmem_ld32(tbase + c * 32, v);
+                const int col0 = n0 + c * 32;
+                if (partial_out) {
+                    float4* dst = reinterpret_cast<float4*>(slot(split) + c * 32);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        __stcg(dst + q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+                    continue;
+                }
+                if (fixup) {
+                    float w[32];
+                    const float4* src0 = reinterpret_cast<const float4*>(slot(0) + c * 32);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const float4 x = __ldcg(src0 + q);
+                        w[4 * q] = x.x, w[4 * q + 1] = x.y, w[4 * q + 2] = x.z, w[4 * q + 3] = x.w;
+                    }
+                    for (int j = 1; j < sp.splits - 1; ++j) {
+                        const float4* srcj = reinterpret_cast<const float4*>(slot(j) + c * 32);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const float4 x = __ldcg(srcj + q);
+                            w[4 * q] += x.x, w[4 * q + 1] += x.y, w[4 * q + 2] += x.z, w[4 * q + 3] += x.w;
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) v[q] = w[q] + v[q];
+                }
+                if (row < M) {
+                    if (col0 + 32 <= N && (N & 3) == 0) {
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            *reinterpret_cast<float4*>(crow + col0 + 4 * q) =
+                                make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                    } else {
+                        for (int q = 0; q < 32; ++q)
+                            if (col0 + q < N) crow[col0 + q] = v[q];
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(empty_leader_base + acc * sizeof(uint64_t));
+            if (partial_out) {    // publish this CTA's partial slot
+                __threadfence();
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (etid == 0) store_release_gpu(flag(split), 1);
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();      // the peer may still be signalling the leader's barriers
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    }
+}
+
 // Pre-pass.  transpose: Bt[n][k] = tf32_rn(B[k][n]).  3xTF32: hi = tf32(x)
 // (cvt.rna), lo = tf32(x - hi); A3 = [A_hi | A_hi | A_lo] (M x 3K) and
 // Bt3 = [B_hi^T | B_lo^T | B_hi^T] (N x 3K), so one tf32 GEMM over 3K sums
@@ -406,11 +715,38 @@ static int make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t
     return HF_OK;
 }
 
+constexpr int PAIR_STAGES = 6;
+
 static const int kRegistered = register_kernels(
-    {(const void*)gemm_tf32_kernel<4, 2>, (const void*)gemm_tf32_kernel<2, 1>, (const void*)transpose_b<true>,
+    {(const void*)gemm_tf32_kernel<4, 2>, (const void*)gemm_tf32_kernel<2, 1>,
+     (const void*)gemm_tf32_pair_kernel<PAIR_STAGES>, (const void*)transpose_b<true>,
      (const void*)transpose_b<false>, (const void*)round_a, (const void*)split3_a});
 
-// Launch shape: persistent (4 stages, double-buffered TMEM, grid = SMs) by
+// HF_GEMM_TC_PAIR=0 selects the single-CTA persistent kernel for standalone
+// calls (A/B comparisons); the default is the CTA-pair kernel.
+static bool pair_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("HF_GEMM_TC_PAIR");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
+
+// HF_GEMM_TC_SPLIT=0 disables the deterministic tail split of the pair kernel.
+static bool split_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("HF_GEMM_TC_SPLIT");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
+
+// Launch shape: CTA pairs (6 stages, double-buffered TMEM, 74 persistent
+// pairs) by default; single-CTA persistent (4 stages, grid = SMs) with
+// HF_GEMM_TC_PAIR=0 or below 256 x 256; co-scheduling (2 stages, 1
+// accumulator, grid = tiles) with
 // default; co-scheduling (2 stages, 1 accumulator, grid = tiles) with
 // HF_GEMM_COSCHEDULE, when the TC replica runs concurrently with the SIMT
 // replica on the same GPU.
@@ -418,6 +754,50 @@ static const int kRegistered = register_kernels(
 static int launch(const float* A, const float* Bt, float* C, int M, int N, int K, int device, cudaStream_t st,
                   bool cosched) {
     CUtensorMap ta, tb;
+    if (!cosched && pair_enabled() && M >= PBM && N >= PBN) {
+        // CTA pairs: each CTA stages half of the 256 x 256 tile's operands
+        int rc = make_map(&ta, A, static_cast<uint64_t>(K), static_cast<uint64_t>(M), static_cast<uint64_t>(K) * 4,
+                          BK, PBM / 2);
+        if (rc) return rc;
+        rc = make_map(&tb, Bt, static_cast<uint64_t>(K), static_cast<uint64_t>(N), static_cast<uint64_t>(K) * 4, BK,
+                      PBN / 2);
+        if (rc) return rc;
+        static bool pair_attr[64] = {false};
+        if (!pair_attr[device]) {
+            HF_CUDA_CHECK(cudaFuncSetAttribute(gemm_tf32_pair_kernel<PAIR_STAGES>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               pair_smem_bytes<PAIR_STAGES>()));
+            pair_attr[device] = true;
+        }
+        const int ptiles = ((M + PBM - 1) / PBM) * ((N + PBN - 1) / PBN);
+        const int pairs_max = num_sms(device) / 2;
+        const int pairs = ptiles < pairs_max ? ptiles : pairs_max;
+        PairSplit sp{ptiles, 1, nullptr, nullptr};
+        const int R = ptiles % pairs;
+        const int nkb = (K + BK - 1) / BK;
+        if (R > 0 && ptiles > pairs && split_enabled()) {
+            int splits = pairs / R;
+            if (splits > 4) splits = 4;
+            if (splits > nkb) splits = nkb;
+            if (splits > 1) {
+                sp.full_tiles = ptiles - R;
+                sp.splits = splits;
+                const size_t slots = static_cast<size_t>(R) * (splits - 1);
+                const size_t pbytes = slots * PBM * PBN * sizeof(float);
+                const size_t fbytes = slots * 2 * sizeof(int);
+                uint8_t* ws = nullptr;
+                HF_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&ws), pbytes + fbytes, st));
+                sp.partial = reinterpret_cast<float*>(ws);
+                sp.flags = reinterpret_cast<int*>(ws + pbytes);
+                HF_CUDA_CHECK(cudaMemsetAsync(sp.flags, 0, fbytes, st));
+            }
+        }
+        gemm_tf32_pair_kernel<PAIR_STAGES><<<2 * pairs, NUM_THREADS, pair_smem_bytes<PAIR_STAGES>(), st>>>(
+            ta, tb, C, M, N, K, sp);
+        if (sp.partial) cudaFreeAsync(sp.partial, st);
+        HF_CHECK_LAUNCH();
+        return HF_OK;
+    }
     int rc = make_map(&ta, A, static_cast<uint64_t>(K), static_cast<uint64_t>(M), static_cast<uint64_t>(K) * 4, BK, BM);
     if (rc) return rc;
     rc = make_map(&tb, Bt, static_cast<uint64_t>(K), static_cast<uint64_t>(N), static_cast<uint64_t>(K) * 4, BK, BN);

@@ -346,6 +346,50 @@ def test_gemm_tc_within_delta(K, shape, mode):
     _agree(got, ref, 1e-3 if (mode & 0xF) == 0 else 1e-4)
 
 
+# CTA-pair kernel (cta_group::2, the default standalone launch shape) with
+# its deterministic tail split: 2560x4096 gives 160 pair tiles over 74 pairs,
+# the 12 tail tiles cut into 4 k-ranges; 4096^2 gives 34 tail tiles in 2.
+@pytest.mark.parametrize("shape", [(2560, 4096, 1024), (4096, 4096, 4096), (300, 520, 264), (1280, 768, 96)])
+def test_gemm_tc_pair_split_matches_single_cta(K, shape):
+    import os
+    import subprocess
+    import sys
+    M, N, Kd = shape
+    rng = np.random.default_rng(M + N + Kd)
+    a = rng.uniform(1, 2, (M, Kd)).astype(np.float32)
+    b = rng.uniform(1, 2, (Kd, N)).astype(np.float32)
+    c = torch.empty(M, N, dtype=torch.float32, device="cuda")
+    K.gemm_tc(dev(a), dev(b), c)
+    c2 = torch.empty_like(c)
+    K.gemm_tc(dev(a), dev(b), c2)
+    torch.cuda.synchronize()
+    got = c.cpu().numpy()
+    assert c2.cpu().numpy().tobytes() == got.tobytes()         # run-to-run identical
+    _agree(got, omatmul.matmul(a, b))
+    # the single-CTA persistent kernel (HF_GEMM_TC_PAIR=0, read once per
+    # process, hence a child process) agrees within the tf32 rounding of the
+    # split's different summation order
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, numpy as np, torch; sys.path.insert(0, %r); "
+            "from paper_1405_2912_b200 import kernels as K; "
+            "a = torch.from_numpy(np.load(sys.argv[1])).cuda(); b = torch.from_numpy(np.load(sys.argv[2])).cuda(); "
+            "c = torch.empty(a.shape[0], b.shape[1], device='cuda'); K.gemm_tc(a, b, c); "
+            "np.save(sys.argv[3], c.cpu().numpy())" % root)
+    import tempfile
+    with tempfile.TemporaryDirectory() as td:
+        fa, fb, fc = (os.path.join(td, f) for f in ("a.npy", "b.npy", "c.npy"))
+        np.save(fa, a)
+        np.save(fb, b)
+        env = dict(os.environ, HF_GEMM_TC_PAIR="0")
+        subprocess.run([sys.executable, "-c", code, fa, fb, fc], env=env, check=True, timeout=120)
+        single = np.load(fc)
+    # tolerance: both accumulate the same tf32 products in fp32, in two
+    # summation orders; at K = 4096 that differs by up to ~2e-5 relative
+    # (measured 1.7e-5), well inside the voter's δ = 1e-3
+    rel = np.abs(single.astype(np.float64) - got) / np.abs(got.astype(np.float64))
+    assert rel.max() < 1e-4, rel.max()
+
+
 def test_gemm_tc_general_signs(K):
     """N(0,1) operands: |err| <= 2^-9 * (|A|·|B|) elementwise (tf32 keeps 10
     mantissa bits per operand; fp32 accumulation)."""
