@@ -9,6 +9,7 @@
 
 #include <mutex>
 #include <string.h>
+#include <stdlib.h>
 
 namespace hf {
 
@@ -133,6 +134,12 @@ cudaError_t end_side_launch(SideStream* side, cudaStream_t st) {
         side->unlock();
     }
     return e;
+}
+
+// HF_PDL=0 launches every PDL-capable kernel the classic way (A/B timing).
+bool pdl_enabled() {
+    static const int on = getenv("HF_PDL") == nullptr || getenv("HF_PDL")[0] != '0';
+    return on != 0;
 }
 
 void retain_scratch_pool(int device) {

@@ -70,6 +70,30 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 int elem_size(int dtype);  // bytes per element or -1
 
+// Launch with programmatic stream serialisation (PDL): the grid may become
+// resident while the stream's previous kernel drains; the kernel itself must
+// execute griddepcontrol.wait before touching memory that kernel produced.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+    if (!pdl_enabled()) {
+        kernel<<<grid, block, smem, st>>>(static_cast<KArgs>(args)...);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 }  // namespace hf
 
 #define HF_CUDA_CHECK(expr)                                                        \
@@ -102,6 +126,11 @@ int elem_size(int dtype);  // bytes per element or -1
 
 // ---- device utilities ----------------------------------------------------
 namespace hf {
+
+// PDL: wait for the previous grid of the stream (no-op without PDL launch).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// PDL: let the stream's next grid start launching.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // 128-bit streaming load that does not allocate in L1 (read-once data).
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {

@@ -49,6 +49,7 @@ __global__ void __launch_bounds__(256) stream_kernel(uint4* __restrict__ dst, co
     const long long gs = static_cast<long long>(gridDim.x) * blockDim.x;
     unsigned long long acc = 0;
     long long j = gtid;
+    pdl_wait();     // launched with PDL: the previous grid's writes are visible from here
     for (; j + (U - 1) * gs < nvec; j += U * gs) {
         uint4 v[U];
 #pragma unroll
@@ -64,6 +65,7 @@ __global__ void __launch_bounds__(256) stream_kernel(uint4* __restrict__ dst, co
         if constexpr (kStore) st_stream(dst + j, v);
         if constexpr (kSum) acc += mix_vec(v, static_cast<unsigned long long>(j) * 4);
     }
+    pdl_launch_dependents();
     // ragged tail (< 16 bytes, or everything when unaligned): per byte copy,
     // per word checksum
     const long long tail0 = nvec * 16;
@@ -116,14 +118,14 @@ static int launch_stream(void* dst, const void* src, long long nbytes, unsigned 
     auto sb = static_cast<const uint8_t*>(src);
     auto db = static_cast<uint8_t*>(dst);
     if (dst && sum) {
-        if (peer_src) stream_kernel<true, true, true><<<grid, 256, 0, st>>>(d4, s4, nvec, sb, db, nbytes, sum);
-        else stream_kernel<true, true, false><<<grid, 256, 0, st>>>(d4, s4, nvec, sb, db, nbytes, sum);
+        if (peer_src) HF_CUDA_CHECK(launch_pdl(stream_kernel<true, true, true>, dim3(grid), dim3(256), 0, st, d4, s4, nvec, sb, db, nbytes, sum));
+        else HF_CUDA_CHECK(launch_pdl(stream_kernel<true, true, false>, dim3(grid), dim3(256), 0, st, d4, s4, nvec, sb, db, nbytes, sum));
     } else if (dst) {
-        if (peer_src) stream_kernel<true, false, true><<<grid, 256, 0, st>>>(d4, s4, nvec, sb, db, nbytes, sum);
-        else stream_kernel<true, false, false><<<grid, 256, 0, st>>>(d4, s4, nvec, sb, db, nbytes, sum);
+        if (peer_src) HF_CUDA_CHECK(launch_pdl(stream_kernel<true, false, true>, dim3(grid), dim3(256), 0, st, d4, s4, nvec, sb, db, nbytes, sum));
+        else HF_CUDA_CHECK(launch_pdl(stream_kernel<true, false, false>, dim3(grid), dim3(256), 0, st, d4, s4, nvec, sb, db, nbytes, sum));
     } else {
-        if (peer_src) stream_kernel<false, true, true><<<grid, 256, 0, st>>>(d4, s4, nvec, sb, db, nbytes, sum);
-        else stream_kernel<false, true, false><<<grid, 256, 0, st>>>(d4, s4, nvec, sb, db, nbytes, sum);
+        if (peer_src) HF_CUDA_CHECK(launch_pdl(stream_kernel<false, true, true>, dim3(grid), dim3(256), 0, st, d4, s4, nvec, sb, db, nbytes, sum));
+        else HF_CUDA_CHECK(launch_pdl(stream_kernel<false, true, false>, dim3(grid), dim3(256), 0, st, d4, s4, nvec, sb, db, nbytes, sum));
     }
     HF_CHECK_LAUNCH();
     return HF_OK;

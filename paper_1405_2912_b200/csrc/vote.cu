@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
     // previous kernel of the stream has finished (its launch and CTA
     // rasterisation overlap that kernel's tail); nothing is read before the
     // previous grid has completed and flushed.
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    pdl_wait();
 
     // ---- vector loop: UNROLL x K 128-bit loads in flight per thread ----
     long long j = gtid;
@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
     }
 
     // the next kernel of the stream may start launching while this grid reduces
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    pdl_launch_dependents();
 
     // ---- reduction: warp -> block (smem) -> one atomic per block ----------
     __shared__ unsigned long long s_cnt[K + 1];
@@ -723,24 +723,9 @@ static int launch_vote(VoteParams& p, int K, int dtype, int width, int device, c
         static const int legacy = getenv("HF_VOTE_GRID_LEGACY") != nullptr;   // A/B timing only
         long long cap = static_cast<long long>(sms) * (legacy ? 8 : resident_ctas(reinterpret_cast<const void*>(k), device));
         int grid = static_cast<int>(want < cap ? want : cap);
-        // programmatic dependent launch (HF_VOTE_PDL=0 disables, A/B only):
+        // programmatic dependent launch (HF_PDL=0 disables, A/B only):
         // back-to-back 64 MiB K=2 votes 23.5 -> 21.7 us (tools/vote_ab.py)
-        static const int pdl = getenv("HF_VOTE_PDL") == nullptr || getenv("HF_VOTE_PDL")[0] != '0';
-        if (pdl) {
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(grid);
-            cfg.blockDim = dim3(threads);
-            cfg.dynamicSmemBytes = 0;
-            cfg.stream = st;
-            cudaLaunchAttribute at[1];
-            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-            at[0].val.programmaticStreamSerializationAllowed = 1;
-            cfg.attrs = at;
-            cfg.numAttrs = 1;
-            HF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k, p));
-        } else {
-            k<<<grid, threads, 0, st>>>(p);
-        }
+        HF_CUDA_CHECK(launch_pdl(k, dim3(grid), dim3(threads), 0, st, p));
     } else {
         long long cap = static_cast<long long>(sms) * 8;
         int grid = static_cast<int>(want < cap ? want : cap);

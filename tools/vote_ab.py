@@ -1,6 +1,6 @@
 """Back-to-back hf_vote_async device time (CUDA events), f32, several sizes
 and K: the launch configuration under test comes from the environment
-(HF_VOTE_PDL).  Prints one JSON line per case."""
+(HF_PDL).  Prints one JSON line per case."""
 import json, os, sys
 from pathlib import Path
 import torch
@@ -25,6 +25,6 @@ for mib, K in ((16, 2), (64, 2), (64, 3), (256, 3), (1024, 3), (1024, 5)):
     st.synchronize()
     t = e0.elapsed_time(e1) / iters * 1e-3
     assert ws.read().verdict == "match"
-    print(json.dumps({"pdl": os.environ.get("HF_VOTE_PDL", "1"),
+    print(json.dumps({"pdl": os.environ.get("HF_PDL", "1"),
                       "mib": mib, "K": K, "us": round(t * 1e6, 2), "read_GBps": round(K * n * 4 / t / 1e9, 1)}))
     del reps, base
