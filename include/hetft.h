@@ -175,13 +175,25 @@ int hf_debug_spin(const int* flag, int64_t max_ns, int device, void* stream);
 
 /* ---- matmul kernel variants (row-major fp32, C = A·B) -------------------- */
 /* tcgen05.mma kind::tf32 with TMA-fed, 128B-swizzled smem and TMEM
- * accumulators.  Requires M % 128 == 0, N % 128 == 0, K % 32 == 0. */
+ * accumulators (CTA pairs, cta_group::2, when standalone).  Any M, N, K >= 1
+ * with N % 4 == 0, K % 4 == 0 and 16-byte aligned operands (TMA); ragged
+ * tiles are zero-filled by TMA and stored masked.  mode: HF_GEMM_TF32 or
+ * HF_GEMM_3XTF32, optionally | HF_GEMM_COSCHEDULE. */
 int hf_gemm_tc(const float* A, const float* B, float* C, int M, int N, int K,
                int mode, int device, void* stream);
 /* Register-tiled FP32 FFMA (no tensor cores). Any M, N, K >= 1.
  * mode: 0 or HF_GEMM_COSCHEDULE. */
 int hf_gemm_simt(const float* A, const float* B, float* C, int M, int N, int K,
                  int mode, int device, void* stream);
+
+/* ---- GPU bodies of the reference's 1-D workloads ------------------------- */
+/* src/hetrt/workloads.py:24-28 (inc; buggy-inc = inc over n-1 elements,
+ * :53-58): dst[i] = src[i] + 1.0f. */
+int hf_vec_inc(const float* src, float* dst, int64_t n, int device, void* stream);
+/* src/hetrt/workloads.py:35-42 (pathfinder-like): dst[i] = a[i] +
+ * min(a[i-1], a[i], a[i+1]) with the ends clamped, np.minimum NaN rules.
+ * src and dst must not alias. */
+int hf_vec_path(const float* src, float* dst, int64_t n, int device, void* stream);
 
 #ifdef __cplusplus
 }

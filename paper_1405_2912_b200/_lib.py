@@ -42,7 +42,7 @@ EXPORTED = (
     "hf_vote", "hf_vote_workspace_bytes", "hf_vote_workspace_init", "hf_vote_async",
     "hf_vote_bytes", "hf_copy", "hf_fill", "hf_checkpoint", "hf_restore", "hf_checksum",
     "hf_inject_bitflip", "hf_inject_scale", "hf_scribble", "hf_gemm_tc", "hf_gemm_simt",
-    "hf_debug_spin",
+    "hf_debug_spin", "hf_vec_inc", "hf_vec_path",
 )
 
 
@@ -99,6 +99,8 @@ def _declare(lib):
                                  _c_void_p]),
         "hf_copy": (_i32, [_c_void_p, _i32, _c_void_p, _i32, _i64, _c_void_p]),
         "hf_fill": (_i32, [_c_void_p, _i32, _i64, _i32, _c_void_p]),
+        "hf_vec_inc": (_i32, [_c_void_p, _c_void_p, _i64, _i32, _c_void_p]),
+        "hf_vec_path": (_i32, [_c_void_p, _c_void_p, _i64, _i32, _c_void_p]),
         "hf_checkpoint": (_i32, [_c_void_p, _c_void_p, _i64, P(ctypes.c_uint64), _i32, _c_void_p]),
         "hf_restore": (_i32, [_c_void_p, _c_void_p, _i64, P(ctypes.c_uint64), _i32, _c_void_p]),
         "hf_checksum": (_i32, [_c_void_p, _i64, P(ctypes.c_uint64), _i32, _c_void_p]),

@@ -167,6 +167,7 @@ constexpr int SGEMM_SMEM = S_STAGES * SB_K * (SB_M + SB_N) * 4;
 // 48 KB reservation (tools/cosched_bench.py); at <= 96 KB the TC CTAs are
 // not placed until the SIMT grid drains.
 constexpr int SGEMM_SMEM_COSCHED = 100000;
+constexpr int SGEMM_SMEM_MAX = 227 * 1024;
 
 // A (M x K) -> At (K x M), 32x32 tiles through padded smem.
 __global__ void __launch_bounds__(256) transpose_a(const float* __restrict__ A, float* __restrict__ At, int M, int K) {
@@ -209,6 +210,18 @@ namespace hf {
 // Tile-row group of the grouped CTA order (HF_SGEMM_GROUP, default 16: at
 // 4096^3 the resident CTAs then share 16 A panels and ~19 B panels in L2;
 // DRAM reads 333 MB with 8, 286 MB with 16, 509 MB with 32, same time).
+// Co-scheduling smem reservation per SIMT CTA (HF_SGEMM_COSCHED_SMEM bytes,
+// experiments only; default SGEMM_SMEM_COSCHED).
+static int sgemm_cosched_smem() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("HF_SGEMM_COSCHED_SMEM");
+        int x = e ? atoi(e) : SGEMM_SMEM_COSCHED;
+        v = x >= SGEMM_SMEM && x <= SGEMM_SMEM_MAX ? x : SGEMM_SMEM_COSCHED;
+    }
+    return v;
+}
+
 static int sgemm_group() {
     static int g = -1;
     if (g < 0) {
@@ -235,7 +248,7 @@ extern "C" int hf_gemm_simt(const float* A, const float* B, float* C, int M, int
         static bool attr[64] = {false};
         if (!attr[device]) {
             HF_CUDA_CHECK(cudaFuncSetAttribute(hf::sgemm_128x128, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               hf::SGEMM_SMEM_COSCHED));
+                                               hf::SGEMM_SMEM_MAX));
             attr[device] = true;
         }
         float* At = nullptr;
@@ -251,7 +264,7 @@ extern "C" int hf_gemm_simt(const float* A, const float* B, float* C, int M, int
         hf::transpose_a<<<dim3(K / 32, M / 32), 256, 0, ps>>>(A, At, M, K);
         HF_CUDA_CHECK(hf::end_side_launch(side, st));
         int tiles = (M / hf::SB_M) * (N / hf::SB_N);
-        const int smem = (mode & HF_GEMM_COSCHEDULE) ? hf::SGEMM_SMEM_COSCHED : hf::SGEMM_SMEM;
+        const int smem = (mode & HF_GEMM_COSCHEDULE) ? hf::sgemm_cosched_smem() : hf::SGEMM_SMEM;
         hf::sgemm_128x128<<<tiles, 256, smem, st>>>(At, B, C, M, N, K, hf::sgemm_group());
         cudaFreeAsync(At, st);
     } else {

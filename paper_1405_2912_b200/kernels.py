@@ -402,6 +402,33 @@ def gemm_tc(A: torch.Tensor, B: torch.Tensor, C: torch.Tensor, mode: int = _lib.
     _count(3)           # B^T (+split) pre-pass, A round/split, tcgen05 GEMM
 
 
+def vec_inc(src: torch.Tensor, dst: torch.Tensor, n: Optional[int] = None,
+            stream: Optional[torch.cuda.Stream] = None) -> None:
+    """dst[:n] = src[:n] + 1 (fp32; reference workloads.py:24-28)."""
+    _vec("hf_vec_inc", src, dst, n, stream)
+
+
+def vec_path(src: torch.Tensor, dst: torch.Tensor, n: Optional[int] = None,
+             stream: Optional[torch.cuda.Stream] = None) -> None:
+    """dst[i] = a[i] + min(a[i-1], a[i], a[i+1]), ends clamped (fp32;
+    reference workloads.py:35-42)."""
+    _vec("hf_vec_path", src, dst, n, stream)
+
+
+def _vec(name, src, dst, n, stream):
+    if src.dtype != torch.float32 or dst.dtype != torch.float32:
+        raise ValueError(f"{name}: fp32 buffers expected")
+    if not (src.is_contiguous() and dst.is_contiguous()):
+        raise ValueError(f"{name}: contiguous buffers expected")
+    n = src.numel() if n is None else int(n)
+    if n > src.numel() or n > dst.numel():
+        raise ValueError(f"{name}: n={n} exceeds the buffers")
+    _lib.init()
+    dev = _dev(dst)
+    check(name, getattr(_lib.load(), name)(src.data_ptr(), dst.data_ptr(), n, dev, _stream_ptr(dev, stream)))
+    _count()
+
+
 def debug_spin(max_ns: int, flag: Optional[torch.Tensor] = None, device: int = 0,
                stream: Optional[torch.cuda.Stream] = None) -> None:
     """Launch the bounded spin kernel (a stand-in hung replica for watchdog

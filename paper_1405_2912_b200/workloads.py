@@ -8,8 +8,9 @@ OpenMP/CUDA pair (§IV-D; reference registry workloads.py:61-111):
   mm_tc3x   "gpu-tc3"   tcgen05 3xTF32 (hi/lo split) — a third, numerically
                         distinct variant for single-GPU TMR
 The reference's 1-D tasks (inc, pathfinder-like, buggy-inc; workloads.py:25-58)
-keep their CPU bodies (numpy over pinned host views) and get GPU bodies that
-run on device views, so the reference experiments stay runnable.
+keep their CPU bodies (numpy over pinned host views) and get GPU bodies
+(hf_vec_inc / hf_vec_path, csrc/vector.cu) on device views, bit-equal to the
+numpy bodies, so the reference experiments stay runnable.
 """
 
 from __future__ import annotations
@@ -76,7 +77,8 @@ def _inc_body(ctx):
     if _is_numpy(src):
         np.add(src[:n], np.float32(1.0), out=dst[:n])
     else:
-        dst[:n].copy_(src[:n]).add_(1.0)
+        from . import kernels
+        kernels.vec_inc(src, dst, n, stream=ctx.stream)
 
 
 def _path_body(ctx):
@@ -89,10 +91,8 @@ def _path_body(ctx):
         right = np.concatenate((a[1:], a[-1:]))
         np.add(a, np.minimum(np.minimum(left, a), right), out=dst[:n])
     else:
-        import torch
-        left = torch.cat((a[:1], a[:-1]))
-        right = torch.cat((a[1:], a[-1:]))
-        torch.add(a, torch.minimum(torch.minimum(left, a), right), out=dst[:n])
+        from . import kernels
+        kernels.vec_path(src, dst, n, stream=ctx.stream)
 
 
 def _buggy_inc_body(ctx):
@@ -103,7 +103,8 @@ def _buggy_inc_body(ctx):
     if _is_numpy(src):
         np.add(src[:n - 1], np.float32(1.0), out=dst[:n - 1])
     else:
-        dst[:n - 1].copy_(src[:n - 1]).add_(1.0)
+        from . import kernels
+        kernels.vec_inc(src, dst, n - 1, stream=ctx.stream)
 
 
 def _inc_oracle(data: np.ndarray) -> np.ndarray:

@@ -418,3 +418,35 @@ def test_sliced_vote_equals_unsliced(K):
     voted = torch.empty_like(td[0])
     res = kernels.vote_sliced(td, 1e-3, voted=voted, devices=[0] * K)
     check_vote(res, ovote.vote(reps, 1e-3), voted)
+
+
+# GPU bodies of the reference's 1-D workloads: bit-equal to the numpy bodies
+# (reference workloads.py:24-58), including NaN / ±0 / ±inf and n = 1, 2.
+@pytest.mark.parametrize("n", [1, 2, 3, 1000, 1 << 20, (1 << 20) + 7])
+def test_vector_workloads_match_numpy(K, n):
+    rng = np.random.default_rng(n)
+    a = rng.uniform(1, 2, n).astype(np.float32)
+    if n >= 12:
+        a[[1, 3, 5, 6]] = [np.nan, -0.0, np.inf, -np.inf]
+        a[4] = 0.0
+        a.view(np.uint32)[[8, 10]] = [0x7FC00123, 0x7F800005]     # NaN payloads: quiet, signalling
+        a[9] = -0.0
+    src = dev(a)
+    out = torch.full((n,), 7.0, dtype=torch.float32, device="cuda")
+    K.vec_inc(src, out)
+    torch.cuda.synchronize()
+    assert out.cpu().numpy().tobytes() == (a + np.float32(1.0)).astype(np.float32).tobytes()
+    left = np.concatenate((a[:1], a[:-1]))
+    right = np.concatenate((a[1:], a[-1:]))
+    with np.errstate(invalid="ignore"):
+        ref = (a + np.minimum(np.minimum(left, a), right)).astype(np.float32)
+    K.vec_path(src, out)
+    torch.cuda.synchronize()
+    assert out.cpu().numpy().tobytes() == ref.tobytes()
+    # buggy-inc: the last element keeps its previous value
+    out2 = torch.full((n,), 7.0, dtype=torch.float32, device="cuda")
+    K.vec_inc(src, out2, n - 1)
+    torch.cuda.synchronize()
+    exp = np.full(n, 7.0, np.float32)
+    exp[:n - 1] = a[:n - 1] + np.float32(1.0)
+    assert out2.cpu().numpy().tobytes() == exp.tobytes()
