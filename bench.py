@@ -614,7 +614,7 @@ def kernel_rooflines(device, n, kernels, torch):
 
 def tmr_rate(device, n, fault_prob, seed, steps, warmup, torch):
     """North-star headline shape on one GPU: HetTMR of the three diverse
-    variants (tcgen05 TF32, SIMT FP32, tcgen05 3xTF32) on a 4096^2 fp32
+    variants (tcgen05 TF32, SIMT FP32, tcgen05 3xBF16) on a 4096^2 fp32
     matmul, device-resident inputs checkpointed into HBM, bit-flip faults at
     the same per-replica probability, majority vote (K = 3) corrects a single
     faulty replica.  CUDA-event timed on the runtime's compute stream."""
@@ -672,7 +672,7 @@ def tmr_rate(device, n, fault_prob, seed, steps, warmup, torch):
     torch.cuda.synchronize()
     t = e0.elapsed_time(e1) * 1e-3
     return {"value": steps / t, "unit": "tasks/s", "ms_per_task": 1e3 * t / steps, "steps": steps,
-            "workload": f"HetTMR {n}x{n} fp32 matmul (tcgen05 TF32 + SIMT FP32 + tcgen05 3xTF32 replicas "
+            "workload": f"HetTMR {n}x{n} fp32 matmul (tcgen05 TF32 + SIMT FP32 + tcgen05 3xBF16 replicas "
                         f"on 1 GPU), HBM checkpoint of inputs, bit flips p={fault_prob}/replica, K=3 majority vote",
             "votes": votes, "rounds": rounds}
 

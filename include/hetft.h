@@ -63,6 +63,7 @@ extern "C" {
 /* GEMM modes (hf_gemm_tc; hf_gemm_simt takes only the COSCHEDULE flag) */
 #define HF_GEMM_TF32     0   /* single-pass kind::tf32                       */
 #define HF_GEMM_3XTF32   1   /* error-compensated big+small split (3 passes) */
+#define HF_GEMM_3XBF16   2   /* the same split on bf16 halves, kind::f16 (2x rate) */
 #define HF_GEMM_COSCHEDULE 0x100 /* flag: launch shapes that share SMs with a
                                     concurrent replica of the other variant:
                                     TC 2 stages, 1 tile/CTA, operand pre-pass on
@@ -177,8 +178,8 @@ int hf_debug_spin(const int* flag, int64_t max_ns, int device, void* stream);
 /* tcgen05.mma kind::tf32 with TMA-fed, 128B-swizzled smem and TMEM
  * accumulators (CTA pairs, cta_group::2, when standalone).  Any M, N, K >= 1
  * with N % 4 == 0, K % 4 == 0 and 16-byte aligned operands (TMA); ragged
- * tiles are zero-filled by TMA and stored masked.  mode: HF_GEMM_TF32 or
- * HF_GEMM_3XTF32, optionally | HF_GEMM_COSCHEDULE. */
+ * tiles are zero-filled by TMA and stored masked.  mode: HF_GEMM_TF32,
+ * HF_GEMM_3XTF32 or HF_GEMM_3XBF16, optionally | HF_GEMM_COSCHEDULE. */
 int hf_gemm_tc(const float* A, const float* B, float* C, int M, int N, int K,
                int mode, int device, void* stream);
 /* Register-tiled FP32 FFMA (no tensor cores). Any M, N, K >= 1.

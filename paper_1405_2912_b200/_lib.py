@@ -34,6 +34,7 @@ VERDICT_NAMES = {HF_VERDICT_MATCH: "match", HF_VERDICT_CORRECTED: "corrected",
 
 HF_GEMM_TF32 = 0
 HF_GEMM_3XTF32 = 1
+HF_GEMM_3XBF16 = 2
 HF_GEMM_COSCHEDULE = 0x100
 
 # every symbol include/hetft.h declares (checked by tests/test_capi.py)

@@ -25,6 +25,7 @@
 #include "common.cuh"
 
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <mutex>
 #include <stdlib.h>
 
@@ -34,7 +35,6 @@ namespace tc {
 constexpr int BM = 128;
 constexpr int BN = 256;
 constexpr int BK = 32;          // one 128-byte swizzle row of fp32
-constexpr int UK = 8;           // tf32 UMMA K
 constexpr int A_STAGE = BM * BK * 4;   // 16 KB
 constexpr int B_STAGE = BN * BK * 4;   // 32 KB
 constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
@@ -101,6 +101,36 @@ __device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint64_t a_desc, ui
         : "memory");
 }
 
+__device__ __forceinline__ void tc_mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// Operand kind of a GEMM launch: tf32 (32-bit elements, UMMA K = 8) or bf16
+// (16-bit elements, UMMA K = 16, kind::f16 at twice the tf32 rate).  Either
+// way one 128-byte swizzle row holds BK_BYTES of K, a stage is the same
+// number of bytes, and each UMMA advances the descriptor by 32 bytes.
+template <bool BF16>
+struct OpKind {
+    static constexpr int ELEM = BF16 ? 2 : 4;
+    static constexpr int BKE = 128 / ELEM;          // K elements per stage (one swizzle row)
+    static constexpr uint32_t FMT = BF16 ? 1u : 2u;  // instruction-descriptor A/B format code
+};
+
+template <bool BF16>
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                       uint32_t accumulate) {
+    if constexpr (BF16)
+        tc_mma_bf16(d_tmem, a_desc, b_desc, idesc, accumulate);
+    else
+        tc_mma_tf32(d_tmem, a_desc, b_desc, idesc, accumulate);
+}
+
 // tcgen05.ld 32 lanes x 32 bits, 32 consecutive columns per thread
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     uint32_t r[32];
@@ -132,11 +162,12 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
     return d;
 }
 
-// Instruction descriptor, kind::tf32, fp32 accumulate, A and B K-major.
-__host__ __device__ constexpr uint32_t make_idesc(int M, int N) {
+// Instruction descriptor, kind::tf32 (fmt 2) or kind::f16 with bf16 (fmt 1),
+// fp32 accumulate, A and B K-major.
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N, uint32_t fmt = 2u) {
     return (1u << 4)            // D format f32
-           | (2u << 7)          // A format tf32
-           | (2u << 10)         // B format tf32
+           | (fmt << 7)         // A format
+           | (fmt << 10)        // B format
            | (0u << 15)         // A K-major
            | (0u << 16)         // B K-major (B^T staged by the pre-pass)
            | (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
@@ -155,10 +186,11 @@ struct Barriers {
 // overlaps a tile's epilogue with the next tile's main loop; 1: one tile per
 // CTA, 2 CTAs/SM co-resident, used when the kernel shares the GPU with the
 // SIMT replica so its CTAs fill the SIMT kernel's last wave).
-template <int STAGES, int ACCS>
+template <int STAGES, int ACCS, bool BF16 = false>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, float* __restrict__ C,
                  int M, int N, int K) {
+    using OK = OpKind<BF16>;
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment for the SWIZZLE_128B atoms
     const uint32_t base_u32 = smem_u32(smem_raw);
@@ -171,7 +203,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     const int tiles_m = (M + BM - 1) / BM;
     const int tiles_n = (N + BN - 1) / BN;
     const int num_tiles = tiles_m * tiles_n;
-    const int nkb = (K + BK - 1) / BK;
+    const int nkb = (K + OK::BKE - 1) / OK::BKE;
 
     if (warp == 0 && lane == 0) {
         prefetch_tmap(&tmA);
@@ -210,8 +242,8 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     uint8_t* sa = smem + stage * STAGE_BYTES;
                     uint8_t* sb = sa + A_STAGE;
                     mbar_expect_tx(&bars->full[stage], STAGE_BYTES);
-                    tma_load_2d(sa, &tmA, &bars->full[stage], kb * BK, m0);
-                    tma_load_2d(sb, &tmB, &bars->full[stage], kb * BK, n0);
+                    tma_load_2d(sa, &tmA, &bars->full[stage], kb * OK::BKE, m0);
+                    tma_load_2d(sb, &tmB, &bars->full[stage], kb * OK::BKE, n0);
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -222,7 +254,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     } else if (warp == 1) {
         // ===== MMA issuer =====
         if (lane == 0) {
-            constexpr uint32_t idesc = make_idesc(BM, BN);
+            constexpr uint32_t idesc = make_idesc(BM, BN, OK::FMT);
             int stage = 0;
             uint32_t phase = 0;
             int local = 0;
@@ -238,12 +270,12 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
                     const uint32_t sb = sa + A_STAGE;
 #pragma unroll
-                    for (int kk = 0; kk < BK / UK; ++kk) {
+                    for (int kk = 0; kk < 4; ++kk) {   // 4 UMMAs of 32 bytes of K per 128-byte row
                         // K-major SW128: advance 32 B along the swizzled 128 B row;
                         // SBO = 1 KB between 8-row groups (LBO unused when swizzled)
-                        uint64_t adesc = make_desc(sa + kk * UK * 4, 16, 1024);
-                        uint64_t bdesc = make_desc(sb + kk * UK * 4, 16, 1024);
-                        tc_mma_tf32(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0);
+                        uint64_t adesc = make_desc(sa + kk * 32, 16, 1024);
+                        uint64_t bdesc = make_desc(sb + kk * 32, 16, 1024);
+                        tc_mma<BF16>(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0);
                     }
                     tc_commit(&bars->empty[stage]);
                     if (++stage == STAGES) {
@@ -363,6 +395,20 @@ __device__ __forceinline__ void tc_mma_tf32_pair(uint32_t d_tmem, uint64_t a_des
         : "memory");
 }
 
+template <bool BF16>
+__device__ __forceinline__ void tc_mma_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+    if constexpr (BF16)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+            "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+            : "memory");
+    else
+        tc_mma_tf32_pair(d_tmem, a_desc, b_desc, idesc, accumulate);
+}
+
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
@@ -390,10 +436,11 @@ __device__ __forceinline__ int load_acquire_gpu(const int* p) {
     return v;
 }
 
-template <int STAGES>
+template <int STAGES, bool BF16 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       float* __restrict__ C, int M, int N, int K, PairSplit sp) {
+    using OK = OpKind<BF16>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t base_u32 = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + ((1024 - (base_u32 & 1023)) & 1023);
@@ -410,7 +457,7 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_cons
     const int tiles_m = (M + PBM - 1) / PBM;
     const int tiles_n = (N + PBN - 1) / PBN;
     const int num_tiles = tiles_m * tiles_n;
-    const int nkb = (K + BK - 1) / BK;
+    const int nkb = (K + OK::BKE - 1) / OK::BKE;
     const int tail = num_tiles - sp.full_tiles;
     const int num_units = sp.full_tiles + tail * sp.splits;
     // unit -> (tile, k-block range, split index)
@@ -467,8 +514,8 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_cons
                     const uint32_t sb = sa + A_HALF;
                     const uint32_t full_leader = map_rank(smem_u32(&bars->full[stage]), 0);
                     if (rank == 0) mbar_expect_tx(&bars->full[stage], 2 * P_STAGE);
-                    tma_load_2d_pair(sa, &tmA, full_leader, kb * BK, m0);
-                    tma_load_2d_pair(sb, &tmB, full_leader, kb * BK, n0);
+                    tma_load_2d_pair(sa, &tmA, full_leader, kb * OK::BKE, m0);
+                    tma_load_2d_pair(sb, &tmB, full_leader, kb * OK::BKE, n0);
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -479,7 +526,7 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_cons
     } else if (warp == 1) {
         // ===== MMA issuer (leader only) =====
         if (rank == 0 && lane == 0) {
-            constexpr uint32_t idesc = make_idesc(PBM, PBN);
+            constexpr uint32_t idesc = make_idesc(PBM, PBN, OK::FMT);
             int stage = 0;
             uint32_t phase = 0;
             int local = 0;
@@ -497,10 +544,10 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_cons
                     const uint32_t sa = smem_u32(smem + stage * P_STAGE);
                     const uint32_t sb = sa + A_HALF;
 #pragma unroll
-                    for (int kk = 0; kk < BK / UK; ++kk) {
-                        uint64_t adesc = make_desc(sa + kk * UK * 4, 16, 1024);
-                        uint64_t bdesc = make_desc(sb + kk * UK * 4, 16, 1024);
-                        tc_mma_tf32_pair(d_tmem, adesc, bdesc, idesc, (kb != kb0) | kk);
+                    for (int kk = 0; kk < 4; ++kk) {
+                        uint64_t adesc = make_desc(sa + kk * 32, 16, 1024);
+                        uint64_t bdesc = make_desc(sb + kk * 32, 16, 1024);
+                        tc_mma_pair<BF16>(d_tmem, adesc, bdesc, idesc, (kb != kb0) | kk);
                     }
                     tc_commit_pair(&bars->empty[stage]);      // frees the stage in both CTAs
                     if (++stage == STAGES) {
@@ -675,6 +722,61 @@ __global__ void split3_a(const float* __restrict__ A, float* __restrict__ A3, in
     }
 }
 
+// 3xBF16 pre-pass: x = hi + lo + O(2^-17 |x|) with hi = bf16_rn(x), lo =
+// bf16_rn(x - hi) (x - hi is exact in fp32).  Segments of Kp = K rounded up
+// to 8 elements (16-byte TMA row pitch), zero-padded:
+//   A3[m]  = [A_hi | A_hi | A_lo]      (M x 3Kp bf16)
+//   Bt3[n] = [B_hi^T | B_lo^T | B_hi^T] (N x 3Kp bf16)
+// so one bf16 GEMM over 3Kp sums A_hi·B_hi + A_hi·B_lo + A_lo·B_hi, on the
+// kind::f16 path at twice the tf32 rate (the dropped A_lo·B_lo is ~2^-16).
+__device__ __forceinline__ void bf16_split(float x, __nv_bfloat16& hi, __nv_bfloat16& lo) {
+    hi = __float2bfloat16_rn(x);
+    lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+}
+
+__global__ void __launch_bounds__(256) split3_a_bf16(const float* __restrict__ A, __nv_bfloat16* __restrict__ A3,
+                                                     int M, int K, int Kp) {
+    const long long total = static_cast<long long>(M) * Kp;
+    const __nv_bfloat16 z = __float2bfloat16_rn(0.f);
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long m = i / Kp;
+        const int k = static_cast<int>(i % Kp);
+        __nv_bfloat16 hi = z, lo = z;
+        if (k < K) bf16_split(A[m * K + k], hi, lo);
+        __nv_bfloat16* row = A3 + m * 3LL * Kp;
+        row[k] = hi;
+        row[Kp + k] = hi;
+        row[2LL * Kp + k] = lo;
+    }
+}
+
+__global__ void __launch_bounds__(256) transpose_b_split3_bf16(const float* __restrict__ B,
+                                                               __nv_bfloat16* __restrict__ Bt3, int K, int N,
+                                                               int Kp) {
+    __shared__ float tile[32][33];
+    const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+#pragma unroll
+    for (int r = ty; r < 32; r += 8) {
+        const int k = k0 + r, n = n0 + tx;
+        tile[r][tx] = (k < K && n < N) ? B[static_cast<long long>(k) * N + n] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = ty; r < 32; r += 8) {
+        const int n = n0 + r, k = k0 + tx;
+        if (n < N && k < Kp) {
+            __nv_bfloat16 hi, lo;
+            bf16_split(tile[tx][r], hi, lo);       // zero (k >= K) splits to zeros
+            __nv_bfloat16* row = Bt3 + static_cast<long long>(n) * 3 * Kp;
+            row[k] = hi;
+            row[Kp + k] = lo;
+            row[2LL * Kp + k] = hi;
+        }
+    }
+}
+
 // ---- host side ----------------------------------------------------------------
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -695,7 +797,7 @@ static EncodeFn get_encode() {
 }
 
 static int make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
-                    uint32_t box_inner, uint32_t box_outer) {
+                    uint32_t box_inner, uint32_t box_outer, bool bf16 = false) {
     EncodeFn enc = get_encode();
     if (!enc) {
         set_error("hf_gemm_tc: cuTensorMapEncodeTiled unavailable");
@@ -705,7 +807,8 @@ static int make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t
     cuuint64_t strides[1] = {row_bytes};
     cuuint32_t box[2] = {box_inner, box_outer};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+    CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                     const_cast<void*>(base), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
@@ -719,8 +822,10 @@ constexpr int PAIR_STAGES = 6;
 
 static const int kRegistered = register_kernels(
     {(const void*)gemm_tf32_kernel<4, 2>, (const void*)gemm_tf32_kernel<2, 1>,
-     (const void*)gemm_tf32_pair_kernel<PAIR_STAGES>, (const void*)transpose_b<true>,
-     (const void*)transpose_b<false>, (const void*)round_a, (const void*)split3_a});
+     (const void*)gemm_tf32_pair_kernel<PAIR_STAGES>, (const void*)gemm_tf32_kernel<4, 2, true>,
+     (const void*)gemm_tf32_kernel<2, 1, true>, (const void*)gemm_tf32_pair_kernel<PAIR_STAGES, true>,
+     (const void*)transpose_b<true>, (const void*)transpose_b<false>, (const void*)round_a, (const void*)split3_a,
+     (const void*)split3_a_bf16, (const void*)transpose_b_split3_bf16});
 
 // HF_GEMM_TC_PAIR=0 selects the single-CTA persistent kernel for standalone
 // calls (A/B comparisons); the default is the CTA-pair kernel.
@@ -750,21 +855,23 @@ static bool split_enabled() {
 // default; co-scheduling (2 stages, 1 accumulator, grid = tiles) with
 // HF_GEMM_COSCHEDULE, when the TC replica runs concurrently with the SIMT
 // replica on the same GPU.
-// A: M x K row-major, Bt: N x K row-major (both K-major)
-static int launch(const float* A, const float* Bt, float* C, int M, int N, int K, int device, cudaStream_t st,
+// A: M x K row-major, Bt: N x K row-major (both K-major; K counts elements
+// of the operand kind, row pitch K * ELEM bytes)
+template <bool BF16>
+static int launch(const void* A, const void* Bt, float* C, int M, int N, int K, int device, cudaStream_t st,
                   bool cosched) {
+    using OK = OpKind<BF16>;
+    const uint64_t pitch = static_cast<uint64_t>(K) * OK::ELEM;
     CUtensorMap ta, tb;
     if (!cosched && pair_enabled() && M >= PBM && N >= PBN) {
         // CTA pairs: each CTA stages half of the 256 x 256 tile's operands
-        int rc = make_map(&ta, A, static_cast<uint64_t>(K), static_cast<uint64_t>(M), static_cast<uint64_t>(K) * 4,
-                          BK, PBM / 2);
+        int rc = make_map(&ta, A, static_cast<uint64_t>(K), static_cast<uint64_t>(M), pitch, OK::BKE, PBM / 2, BF16);
         if (rc) return rc;
-        rc = make_map(&tb, Bt, static_cast<uint64_t>(K), static_cast<uint64_t>(N), static_cast<uint64_t>(K) * 4, BK,
-                      PBN / 2);
+        rc = make_map(&tb, Bt, static_cast<uint64_t>(K), static_cast<uint64_t>(N), pitch, OK::BKE, PBN / 2, BF16);
         if (rc) return rc;
         static bool pair_attr[64] = {false};
         if (!pair_attr[device]) {
-            HF_CUDA_CHECK(cudaFuncSetAttribute(gemm_tf32_pair_kernel<PAIR_STAGES>,
+            HF_CUDA_CHECK(cudaFuncSetAttribute(gemm_tf32_pair_kernel<PAIR_STAGES, BF16>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                pair_smem_bytes<PAIR_STAGES>()));
             pair_attr[device] = true;
@@ -774,7 +881,7 @@ static int launch(const float* A, const float* Bt, float* C, int M, int N, int K
         const int pairs = ptiles < pairs_max ? ptiles : pairs_max;
         PairSplit sp{ptiles, 1, nullptr, nullptr};
         const int R = ptiles % pairs;
-        const int nkb = (K + BK - 1) / BK;
+        const int nkb = (K + OK::BKE - 1) / OK::BKE;
         if (R > 0 && ptiles > pairs && split_enabled()) {
             int splits = pairs / R;
             if (splits > 4) splits = 4;
@@ -792,31 +899,31 @@ static int launch(const float* A, const float* Bt, float* C, int M, int N, int K
                 HF_CUDA_CHECK(cudaMemsetAsync(sp.flags, 0, fbytes, st));
             }
         }
-        gemm_tf32_pair_kernel<PAIR_STAGES><<<2 * pairs, NUM_THREADS, pair_smem_bytes<PAIR_STAGES>(), st>>>(
+        gemm_tf32_pair_kernel<PAIR_STAGES, BF16><<<2 * pairs, NUM_THREADS, pair_smem_bytes<PAIR_STAGES>(), st>>>(
             ta, tb, C, M, N, K, sp);
         if (sp.partial) cudaFreeAsync(sp.partial, st);
         HF_CHECK_LAUNCH();
         return HF_OK;
     }
-    int rc = make_map(&ta, A, static_cast<uint64_t>(K), static_cast<uint64_t>(M), static_cast<uint64_t>(K) * 4, BK, BM);
+    int rc = make_map(&ta, A, static_cast<uint64_t>(K), static_cast<uint64_t>(M), pitch, OK::BKE, BM, BF16);
     if (rc) return rc;
-    rc = make_map(&tb, Bt, static_cast<uint64_t>(K), static_cast<uint64_t>(N), static_cast<uint64_t>(K) * 4, BK, BN);
+    rc = make_map(&tb, Bt, static_cast<uint64_t>(K), static_cast<uint64_t>(N), pitch, OK::BKE, BN, BF16);
     if (rc) return rc;
     const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
     static bool attr_set[64] = {false};
     if (!attr_set[device]) {
-        HF_CUDA_CHECK(cudaFuncSetAttribute(gemm_tf32_kernel<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        HF_CUDA_CHECK(cudaFuncSetAttribute(gemm_tf32_kernel<4, 2, BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            smem_bytes<4>()));
-        HF_CUDA_CHECK(cudaFuncSetAttribute(gemm_tf32_kernel<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        HF_CUDA_CHECK(cudaFuncSetAttribute(gemm_tf32_kernel<2, 1, BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            smem_bytes<2>()));
         attr_set[device] = true;
     }
     if (cosched) {
-        gemm_tf32_kernel<2, 1><<<tiles, NUM_THREADS, smem_bytes<2>(), st>>>(ta, tb, C, M, N, K);
+        gemm_tf32_kernel<2, 1, BF16><<<tiles, NUM_THREADS, smem_bytes<2>(), st>>>(ta, tb, C, M, N, K);
     } else {
         const int sms = num_sms(device);
         const int grid = tiles < sms ? tiles : sms;
-        gemm_tf32_kernel<4, 2><<<grid, NUM_THREADS, smem_bytes<4>(), st>>>(ta, tb, C, M, N, K);
+        gemm_tf32_kernel<4, 2, BF16><<<grid, NUM_THREADS, smem_bytes<4>(), st>>>(ta, tb, C, M, N, K);
     }
     HF_CHECK_LAUNCH();
     return HF_OK;
@@ -831,7 +938,8 @@ extern "C" int hf_gemm_tc(const float* A, const float* B, float* C, int M, int N
     HF_REQUIRE(M > 0 && N > 0 && K > 0, "hf_gemm_tc: bad shape %dx%dx%d", M, N, K);
     const bool cosched = (mode & HF_GEMM_COSCHEDULE) != 0;
     mode &= ~HF_GEMM_COSCHEDULE;
-    HF_REQUIRE(mode == HF_GEMM_TF32 || mode == HF_GEMM_3XTF32, "hf_gemm_tc: unknown mode %d", mode);
+    HF_REQUIRE(mode == HF_GEMM_TF32 || mode == HF_GEMM_3XTF32 || mode == HF_GEMM_3XBF16,
+               "hf_gemm_tc: unknown mode %d", mode);
     if (K % 4 != 0 || N % 4 != 0 || (reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) % 16 != 0) {
         hf::set_error("hf_gemm_tc: TMA needs 16-byte aligned operands and K %% 4 == N %% 4 == 0 (got K=%d N=%d)", K, N);
         return HF_EUNSUP;
@@ -840,12 +948,15 @@ extern "C" int hf_gemm_tc(const float* A, const float* B, float* C, int M, int N
     HF_REQUIRE(g.ok, "hf_gemm_tc: cannot select device %d", device);
     cudaStream_t st = hf::as_stream(stream);
     hf::retain_scratch_pool(device);
-    const bool split = mode == HF_GEMM_3XTF32;
-    const int Ke = split ? 3 * K : K;
-    float* Bt = nullptr;
-    float* A3 = nullptr;
-    HF_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&Bt), static_cast<size_t>(N) * Ke * sizeof(float), st));
-    HF_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&A3), static_cast<size_t>(M) * Ke * sizeof(float), st));
+    const bool bf16 = mode == HF_GEMM_3XBF16;
+    const bool split = mode != HF_GEMM_TF32;
+    const int Kp = bf16 ? (K + 7) / 8 * 8 : K;
+    const int Ke = split ? 3 * Kp : K;
+    const size_t elem = bf16 ? 2 : 4;
+    void* Bt = nullptr;
+    void* A3 = nullptr;
+    HF_CUDA_CHECK(cudaMallocAsync(&Bt, static_cast<size_t>(N) * Ke * elem, st));
+    HF_CUDA_CHECK(cudaMallocAsync(&A3, static_cast<size_t>(M) * Ke * elem, st));
     // Co-scheduled with a SIMT replica: the pre-pass runs on a high-priority
     // side stream (level 1: one below the SIMT pre-pass), so its CTAs are
     // dispatched ahead of the SIMT GEMM's pending CTAs, while the GEMM itself
@@ -855,19 +966,25 @@ extern "C" int hf_gemm_tc(const float* A, const float* B, float* C, int M, int N
     hf::SideStream* side = cosched ? hf::side_stream(device, 1) : nullptr;
     cudaStream_t ps = st;
     HF_CUDA_CHECK(hf::begin_side_launch(side, st, &ps));
-    dim3 tgrid((N + 31) / 32, (K + 31) / 32);
-    if (split) {
-        hf::tc::transpose_b<true><<<tgrid, 256, 0, ps>>>(B, Bt, K, N);
-        hf::tc::split3_a<<<hf::num_sms(device) * 8, 256, 0, ps>>>(A, A3, M, K);
+    const int pre_grid = hf::num_sms(device) * 8;
+    if (bf16) {
+        dim3 tgrid((N + 31) / 32, (Kp + 31) / 32);
+        hf::tc::transpose_b_split3_bf16<<<tgrid, 256, 0, ps>>>(B, static_cast<__nv_bfloat16*>(Bt), K, N, Kp);
+        hf::tc::split3_a_bf16<<<pre_grid, 256, 0, ps>>>(A, static_cast<__nv_bfloat16*>(A3), M, K, Kp);
+    } else if (split) {
+        dim3 tgrid((N + 31) / 32, (K + 31) / 32);
+        hf::tc::transpose_b<true><<<tgrid, 256, 0, ps>>>(B, static_cast<float*>(Bt), K, N);
+        hf::tc::split3_a<<<pre_grid, 256, 0, ps>>>(A, static_cast<float*>(A3), M, K);
     } else {
-        hf::tc::transpose_b<false><<<tgrid, 256, 0, ps>>>(B, Bt, K, N);
+        dim3 tgrid((N + 31) / 32, (K + 31) / 32);
+        hf::tc::transpose_b<false><<<tgrid, 256, 0, ps>>>(B, static_cast<float*>(Bt), K, N);
         const long long n4 = static_cast<long long>(M) * K / 4;  // K % 4 == 0
-        hf::tc::round_a<<<hf::num_sms(device) * 8, 256, 0, ps>>>(reinterpret_cast<const float4*>(A),
-                                                                 reinterpret_cast<float4*>(A3), n4);
+        hf::tc::round_a<<<pre_grid, 256, 0, ps>>>(reinterpret_cast<const float4*>(A), static_cast<float4*>(A3), n4);
     }
     HF_CUDA_CHECK(hf::end_side_launch(side, st));
-    int rc = hf::tc::launch(A3, Bt, C, M, N, Ke, device, st, cosched);
+    int rc = bf16 ? hf::tc::launch<true>(A3, Bt, C, M, N, Ke, device, st, cosched)
+                  : hf::tc::launch<false>(A3, Bt, C, M, N, Ke, device, st, cosched);
     cudaFreeAsync(Bt, st);
-    if (A3) cudaFreeAsync(A3, st);
+    cudaFreeAsync(A3, st);
     return rc;
 }

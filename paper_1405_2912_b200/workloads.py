@@ -5,7 +5,8 @@ three diverse GPU variants, attached per unit kind like the paper's
 OpenMP/CUDA pair (§IV-D; reference registry workloads.py:61-111):
   mm_tc     "gpu-tc"    tcgen05.mma kind::tf32, RN-rounded operands
   mm_simt   "gpu-simt"  register-tiled FP32 FFMA (no tensor cores)
-  mm_tc3x   "gpu-tc3"   tcgen05 3xTF32 (hi/lo split) — a third, numerically
+  mm_tc3x   "gpu-tc3"   tcgen05 3xBF16 (bf16 hi/lo split on the kind::f16 path,
+                        twice the tf32 rate; 3xTF32 is HF_GEMM_3XTF32) — a third, numerically
                         distinct variant for single-GPU TMR
 The reference's 1-D tasks (inc, pathfinder-like, buggy-inc; workloads.py:25-58)
 keep their CPU bodies (numpy over pinned host views) and get GPU bodies
@@ -53,8 +54,9 @@ def mm_tc_body(ctx):
 
 def mm_tc3x_body(ctx):
     from . import kernels
+    from ._lib import HF_GEMM_3XBF16
     a, b, c = _mm_views(ctx)
-    kernels.gemm_tc(a, b, c, mode=1 | _tc_flags(ctx), stream=ctx.stream)
+    kernels.gemm_tc(a, b, c, mode=HF_GEMM_3XBF16 | _tc_flags(ctx), stream=ctx.stream)
 
 
 def mm_simt_body(ctx):
@@ -196,7 +198,7 @@ _register(Workload("pathfinder-like", "neighborhood-minimum reduction",
 _register(Workload("buggy-inc", "increment with a deterministic off-by-one bug in the GPU variant",
                    [("inc_ref_cpu", "cpu", _inc_body), ("inc_buggy_gpu", "gpu", _buggy_inc_body)],
                    oracle=_inc_oracle))
-_register(Workload("matmul", "C = A·B, fp32 n x n: tcgen05 TF32 / SIMT FP32 / tcgen05 3xTF32 variants",
+_register(Workload("matmul", "C = A·B, fp32 n x n: tcgen05 TF32 / SIMT FP32 / tcgen05 3xBF16 variants",
                    list(MATMUL_VARIANTS), oracle=_matmul_oracle, params=MATMUL_PARAMS,
                    input_fn=_matmul_input, bind=_matmul_bind))
 

@@ -329,7 +329,7 @@ def test_gemm_simt_rejects_unknown_mode(K):
 
 @pytest.mark.parametrize("shape", [(128, 256, 32), (256, 512, 64), (1024, 1024, 1024),
                                    (2048, 2048, 2048), (200, 100, 36), (384, 136, 4100)])
-@pytest.mark.parametrize("mode", [0, 1, 0x100, 0x101])   # 0x100: co-scheduling launch shape
+@pytest.mark.parametrize("mode", [0, 1, 2, 0x100, 0x101, 0x102])   # 0x100: co-scheduling launch shape
 def test_gemm_tc_within_delta(K, shape, mode):
     M, N, Kd = shape
     rng = np.random.default_rng(M + 7 * N + Kd + mode)
@@ -341,8 +341,9 @@ def test_gemm_tc_within_delta(K, shape, mode):
     got = c.cpu().numpy()
     ref = omatmul.matmul(a, b)
     # tolerance: δ = 1e-3 (voter predicate) for single-pass RN-tf32 operands
-    # on U[1,2) (measured max 4.5e-5 class); 3xTF32 (mode 1) 1e-4 (its error is
-    # dominated by the tensor core's fp32 accumulation, measured 2-4e-5)
+    # on U[1,2) (measured max 4.5e-5 class); 3xTF32 (mode 1) and 3xBF16
+    # (mode 2: 16-bit hi+lo split, dropped lo·lo term ~2^-16) 1e-4 (their
+    # error is dominated by the tensor core's fp32 accumulation, 2-4e-5)
     _agree(got, ref, 1e-3 if (mode & 0xF) == 0 else 1e-4)
 
 

@@ -24,13 +24,25 @@ ap.add_argument("--depth", type=int, default=1)
 ap.add_argument("--nogc", action="store_true")
 ap.add_argument("--noreserve", action="store_true")
 ap.add_argument("--lookahead", type=int, default=2)
+ap.add_argument("--tmr", action="store_true", help="HetTMR (tc, simt, tc3) instead of bench.py's HetDMR")
 ap.add_argument("--device", action="store_true", help="device-resident inputs (bench.py's `value` loop)")
 ap.add_argument("--n", type=int, default=4096)
 ap.add_argument("--profile", action="store_true")
 ap.add_argument("--kineto", default=None, help="write a torch.profiler chrome trace of the timed run here")
 args = ap.parse_args()
 
-hf, rt, task = bench.build_runtime(0, args.p, 1)
+if args.tmr:
+    import paper_1405_2912_b200 as hf
+    kinds = ("gpu-tc", "gpu-simt", "gpu-tc3")
+    cfg = hf.gpu_fleet_config(devices=(0,), kinds=kinds)
+    cfg["memory_spaces"].append({"id": "gpu0ckpt", "device": 0})
+    for i, u in enumerate(cfg["units"]):
+        u.update({"corrupt_prob": args.p, "corrupt_mode": "bitflip", "seed": 1_000_003 + i * 101 + 31})
+    rt = hf.Runtime(hf.load_fleet(cfg), hf.RuntimeConfig(checkpoint_space="gpu0ckpt", serial_replicas=True,
+                                                         attempt_limit=64))
+    task = hf.get_workload("matmul").attach(rt, kinds=kinds)
+else:
+    hf, rt, task = bench.build_runtime(0, args.p, 1)
 n = args.n
 nb = n * n * 4
 space = "gpu0mem"
@@ -38,7 +50,7 @@ hA = (torch.rand(n * n) + 1).view(torch.uint8).pin_memory()
 hB = (torch.rand(n * n) + 1).view(torch.uint8).pin_memory()
 hC = torch.empty(nb, dtype=torch.uint8).pin_memory()
 hZ = torch.zeros(nb, dtype=torch.uint8).pin_memory()
-strat = hf.Strategy(hf.StrategyKind.HET_DMR)
+strat = hf.Strategy(hf.StrategyKind.HET_TMR if args.tmr else hf.StrategyKind.HET_DMR)
 if not args.__dict__.get("noreserve"):
     rt.reserve(space, nb, 24)
 

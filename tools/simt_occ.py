@@ -29,6 +29,12 @@ def run(which, iters=10):
             kernels.gemm_tc(a, b, cs[1], mode=CS, stream=ss[1])
         if "tc3" in which:
             kernels.gemm_tc(a, b, cs[2], mode=1 | CS, stream=ss[2])
+        if "tc3pair" in which:
+            kernels.gemm_tc(a, b, cs[2], mode=1, stream=ss[2])
+        if "bf3" in which:
+            kernels.gemm_tc(a, b, cs[2], mode=2 | CS, stream=ss[2])
+        if "bf3pair" in which:
+            kernels.gemm_tc(a, b, cs[2], mode=2, stream=ss[2])
         for s in ss:
             main.wait_stream(s)
         t1.record(main)
@@ -39,6 +45,7 @@ def run(which, iters=10):
 
 
 out = {"smem": os.environ.get("HF_SGEMM_COSCHED_SMEM", "100000")}
-for w in (("simt",), ("tc",), ("tc3",), ("simt", "tc"), ("simt", "tc", "tc3")):
+for w in (("simt",), ("tc",), ("tc3",), ("tc3pair",), ("bf3",), ("bf3pair",), ("simt", "tc"),
+          ("simt", "tc", "tc3"), ("simt", "tc", "bf3")):
     out["+".join(w)] = run(w)
 print(json.dumps(out))

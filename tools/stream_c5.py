@@ -4,7 +4,7 @@ fault injection and checkpoint rollback, sharded over the GPUs of one box.
 Each rank (one process per GPU, launched by torchrun for N > 1) owns the
 tasks t with t mod world == rank (sharding.tasks_for_rank) and runs them
 through the drop-in Runtime's TaskStream on its own GPU: HetTMR of the three
-diverse variants (tcgen05 TF32, SIMT FP32, tcgen05 3xTF32; one logical unit
+diverse variants (tcgen05 TF32, SIMT FP32, tcgen05 3xBF16; one logical unit
 each, sharing the GPU's memory space), protected attempts checkpoint their
 device-resident inputs into an HBM reserve space, every unit draws faults
 from its own seeded stream — bit-flip corruption (caught or masked by the
