@@ -103,6 +103,7 @@ sgemm_128x128(const float* __restrict__ At, const float* __restrict__ B, float* 
         for (int j = 0; j < 4; ++j) acc[i][j] = 0ull;
 
     const int nk = K / SB_K;
+    pdl_wait();     // launched with PDL behind the A^T pre-pass: At is complete from here
 #pragma unroll
     for (int s = 0; s < S_STAGES - 1; ++s) {
         if (s < nk) issue(s, s);
@@ -172,6 +173,8 @@ constexpr int SGEMM_SMEM_MAX = 227 * 1024;
 // A (M x K) -> At (K x M), 32x32 tiles through padded smem.
 __global__ void __launch_bounds__(256) transpose_a(const float* __restrict__ A, float* __restrict__ At, int M, int K) {
     __shared__ float tile[32][33];
+    pdl_wait();                 // A may come from the previous kernel of the stream
+    pdl_launch_dependents();    // the GEMM may launch (and wait) while this pass drains
     const int m0 = blockIdx.y * 32, k0 = blockIdx.x * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
 #pragma unroll
@@ -207,9 +210,6 @@ static const int kRegistered =
 }  // namespace hf
 
 namespace hf {
-// Tile-row group of the grouped CTA order (HF_SGEMM_GROUP, default 16: at
-// 4096^3 the resident CTAs then share 16 A panels and ~19 B panels in L2;
-// DRAM reads 333 MB with 8, 286 MB with 16, 509 MB with 32, same time).
 // Co-scheduling smem reservation per SIMT CTA (HF_SGEMM_COSCHED_SMEM bytes,
 // experiments only; default SGEMM_SMEM_COSCHED).
 static int sgemm_cosched_smem() {
@@ -220,6 +220,14 @@ static int sgemm_cosched_smem() {
         v = x >= SGEMM_SMEM && x <= SGEMM_SMEM_MAX ? x : SGEMM_SMEM_COSCHED;
     }
     return v;
+}
+
+// Tile-row group of the grouped CTA order (HF_SGEMM_GROUP, default 16: at
+// 4096^3 the resident CTAs then share 16 A panels and ~19 B panels in L2;
+// DRAM reads 333 MB with 8, 286 MB with 16, 509 MB with 32, same time).
+static bool simt_pdl() {
+    static const int on = getenv("HF_SIMT_PDL") != nullptr && getenv("HF_SIMT_PDL")[0] == '1';
+    return on != 0 && pdl_enabled();
 }
 
 static int sgemm_group() {
@@ -258,14 +266,24 @@ extern "C" int hf_gemm_simt(const float* A, const float* B, float* C, int M, int
         // so this GEMM's grid is pending before the TC GEMM's and, launched on
         // the executor's higher-priority lead stream, is dispatched first; the
         // TC CTAs then fill its last wave.
-        hf::SideStream* side = (mode & HF_GEMM_COSCHEDULE) ? hf::side_stream(device, 0) : nullptr;
-        cudaStream_t ps = st;
-        HF_CUDA_CHECK(hf::begin_side_launch(side, st, &ps));
-        hf::transpose_a<<<dim3(K / 32, M / 32), 256, 0, ps>>>(A, At, M, K);
-        HF_CUDA_CHECK(hf::end_side_launch(side, st));
         int tiles = (M / hf::SB_M) * (N / hf::SB_N);
         const int smem = (mode & HF_GEMM_COSCHEDULE) ? hf::sgemm_cosched_smem() : hf::SGEMM_SMEM;
-        hf::sgemm_128x128<<<tiles, 256, smem, st>>>(At, B, C, M, N, K, hf::sgemm_group());
+        if (hf::simt_pdl()) {
+            // HF_SIMT_PDL=1: A^T pre-pass and GEMM on the caller's stream, the
+            // GEMM launched with PDL (no launch gap after the pre-pass).  Off
+            // by default: co-scheduled with a TC replica the TC GEMM then got
+            // SMs at the start of the SIMT grid, 2.46 -> 2.49 ms per DMR round
+            HF_CUDA_CHECK(hf::launch_pdl(hf::transpose_a, dim3(K / 32, M / 32), dim3(256), 0, st, A, At, M, K));
+            HF_CUDA_CHECK(hf::launch_pdl(hf::sgemm_128x128, dim3(tiles), dim3(256), smem, st, At, B, C, M, N, K,
+                                         hf::sgemm_group()));
+        } else {
+            hf::SideStream* side = (mode & HF_GEMM_COSCHEDULE) ? hf::side_stream(device, 0) : nullptr;
+            cudaStream_t ps = st;
+            HF_CUDA_CHECK(hf::begin_side_launch(side, st, &ps));
+            hf::transpose_a<<<dim3(K / 32, M / 32), 256, 0, ps>>>(A, At, M, K);
+            HF_CUDA_CHECK(hf::end_side_launch(side, st));
+            hf::sgemm_128x128<<<tiles, 256, smem, st>>>(At, B, C, M, N, K, hf::sgemm_group());
+        }
         cudaFreeAsync(At, st);
     } else {
         dim3 grid((N + 15) / 16, (M + 15) / 16);
