@@ -65,7 +65,9 @@ def mm_simt_body(ctx):
     kernels.gemm_simt(a, b, c, mode=_tc_flags(ctx), stream=ctx.stream)
 
 
-MATMUL_PARAMS = (Param.area("A", "r"), Param.area("B", "r"), Param.area("C", "w"), Param.scalar("n"))
+# every matmul variant writes all of C: its provisional buffers skip the zero fill
+MATMUL_PARAMS = (Param.area("A", "r"), Param.area("B", "r"), Param.area("C", "w", overwrites=True),
+                 Param.scalar("n"))
 MATMUL_VARIANTS = (("mm_tc", "gpu-tc", mm_tc_body), ("mm_simt", "gpu-simt", mm_simt_body),
                    ("mm_tc3x", "gpu-tc3", mm_tc3x_body))
 

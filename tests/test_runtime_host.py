@@ -499,3 +499,23 @@ class TestTaskStream:
                 reps.append(ts.submit(task, a, DMR))
         seqs = [log["seq"] for r in reps for log in r.rounds_log]
         assert seqs == sorted(seqs) and len(set(seqs)) == len(seqs)
+
+
+def test_overwrite_area_skips_zero_fill_only_when_declared():
+    """Param.area(..., overwrites=True) (new) leaves a "w" provisional buffer
+    uninitialised; plain "w" keeps the reference's zeroed buffer
+    (memory.py:168), and overwrites is rejected for r/rw areas."""
+    with pytest.raises(hf.DeclarationError):
+        hf.Param.area("x", "rw", overwrites=True)
+    calls = []
+
+    class Spy(HostBackend):
+        def alloc(self, space, nbytes, zero=True):
+            calls.append(zero)
+            return super().alloc(space, nbytes, zero)
+
+    m = hf.MemoryManager(hf.load_fleet(three_units()), Spy())
+    a = m.register(bytes(16), 4, hf.ValueType.FLOAT32, "w")
+    m.request(a, "host", "w", protect=False)
+    m.request(a, "host", "w", protect=False, zero_fill=False)
+    assert calls == [True, False]
