@@ -177,17 +177,29 @@ def reference_tasks(n: int, count_or_seconds, seed: int, by_time: bool):
             c1 = a @ b
             ovote.vote([c0, c1], 1e-3)
         kind, detail = "port", "oracle port: 2 numpy matmuls + oracle.vote (reference absent)"
-    t0 = time.perf_counter()
-    done = 0
-    while True:
-        one()
-        done += 1
-        el = time.perf_counter() - t0
-        if by_time and el >= count_or_seconds and done >= 1:
-            break
-        if not by_time and done >= count_or_seconds:
-            break
-    return done, time.perf_counter() - t0, kind, detail
+    # all host cores for the BLAS matmul bodies: torchrun exports
+    # OMP_NUM_THREADS=1 to every rank, which would leave the reference arm
+    # single-threaded under the driver's multi-GPU launch
+    try:
+        from threadpoolctl import threadpool_limits
+        limiter = threadpool_limits(limits=host_cores(), user_api="blas")
+    except Exception:  # noqa: BLE001 - threadpoolctl absent: numpy's own default
+        limiter = None
+    try:
+        t0 = time.perf_counter()
+        done = 0
+        while True:
+            one()
+            done += 1
+            el = time.perf_counter() - t0
+            if by_time and el >= count_or_seconds and done >= 1:
+                break
+            if not by_time and done >= count_or_seconds:
+                break
+        return done, time.perf_counter() - t0, kind, detail
+    finally:
+        if limiter is not None:
+            limiter.restore_original_limits()
 
 
 def host_cores() -> int:
@@ -237,8 +249,14 @@ def run_hetft_arm(args, rank, world, local):
 
     device = local if torch.cuda.device_count() > local else 0
     torch.cuda.set_device(device)
+    # one GPU per rank: NCCL for the barrier and the max over ranks; more
+    # ranks than GPUs (a code-path check on a small box) falls back to gloo
+    shared_gpu = torch.cuda.device_count() < world
     if world > 1 and not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{device}"))
+        if shared_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{device}"))
 
     def barrier():
         if world > 1:
@@ -247,7 +265,7 @@ def run_hetft_arm(args, rank, world, local):
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{device}")
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if shared_gpu else f"cuda:{device}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 

@@ -64,8 +64,12 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dev = local if torch.cuda.device_count() > local else 0
     torch.cuda.set_device(dev)
+    shared_gpu = torch.cuda.device_count() < world      # code-path check: ranks share a GPU -> gloo
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
+        if shared_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
 
     n, nn = args.n, args.n * args.n
     kinds = ("gpu-tc", "gpu-simt", "gpu-tc3") if args.strategy == "hettmr" else ("gpu-tc", "gpu-simt")
@@ -150,8 +154,9 @@ def main():
     wall = time.perf_counter() - w0
     t_dev = e0.elapsed_time(e1) * 1e-3
     keys = sorted(cnt)
-    vec = torch.tensor([cnt[k] for k in keys], dtype=torch.int64, device=d)
-    tmax = torch.tensor([t_dev], dtype=torch.float64, device=d)
+    cd = "cpu" if shared_gpu else d
+    vec = torch.tensor([cnt[k] for k in keys], dtype=torch.int64, device=cd)
+    tmax = torch.tensor([t_dev], dtype=torch.float64, device=cd)
     if world > 1:
         dist.barrier()
         dist.all_reduce(vec)
