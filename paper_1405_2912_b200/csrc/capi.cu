@@ -8,6 +8,8 @@
 #include <vector>
 
 #include <mutex>
+#include <map>
+#include <tuple>
 #include <string.h>
 #include <stdlib.h>
 
@@ -112,6 +114,28 @@ SideStream* side_stream(int device, int level) {
             s->stream = nullptr;
     });
     return s->stream ? s : nullptr;
+}
+
+void* stream_scratch(int device, cudaStream_t st, int slot, size_t bytes) {
+    struct Buf {
+        void* ptr = nullptr;
+        size_t bytes = 0;
+    };
+    static std::mutex mu;
+    static std::map<std::tuple<int, cudaStream_t, int>, Buf> bufs;
+    std::lock_guard<std::mutex> lk(mu);
+    Buf& b = bufs[std::make_tuple(device, st, slot)];
+    if (b.bytes < bytes) {
+        if (b.ptr) cudaFreeAsync(b.ptr, st);
+        b.ptr = nullptr;
+        b.bytes = 0;
+        if (cudaMallocAsync(&b.ptr, bytes, st) != cudaSuccess) {
+            b.ptr = nullptr;
+            return nullptr;
+        }
+        b.bytes = bytes;
+    }
+    return b.ptr;
 }
 
 cudaError_t begin_side_launch(SideStream* side, cudaStream_t st, cudaStream_t* launch_stream) {

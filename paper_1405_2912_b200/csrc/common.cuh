@@ -37,6 +37,13 @@ struct SideStream {
     void unlock();
 };
 SideStream* side_stream(int device, int level);
+
+// Stream-ordered scratch owned per (device, stream, slot): reused by every
+// later call on the same stream (stream order makes reuse safe), grown with
+// cudaMallocAsync/cudaFreeAsync on that stream when a call needs more.  Saves
+// the per-call allocate/free pair of the GEMM pre-passes.  Never freed (the
+// process owns a few per unit stream).  Returns nullptr on failure.
+void* stream_scratch(int device, cudaStream_t st, int slot, size_t bytes);
 // begin: lock + fork, *launch_stream = side stream (or `st` when side is
 // NULL).  end: check the launches, join back into `st`, unlock.  Both return
 // the first CUDA error; end always unlocks.

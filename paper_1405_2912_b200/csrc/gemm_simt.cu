@@ -259,8 +259,11 @@ extern "C" int hf_gemm_simt(const float* A, const float* B, float* C, int M, int
                                                hf::SGEMM_SMEM_MAX));
             attr[device] = true;
         }
-        float* At = nullptr;
-        HF_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&At), static_cast<size_t>(M) * K * sizeof(float), st));
+        float* At = static_cast<float*>(hf::stream_scratch(device, st, 2, static_cast<size_t>(M) * K * sizeof(float)));
+        if (!At) {
+            hf::set_error("hf_gemm_simt: cannot allocate the A^T scratch");
+            return HF_ECUDA;
+        }
         // Co-scheduled: the A^T pre-pass runs on the device's greatest-priority
         // side stream, ahead of the tensor-core replica's pre-pass (level 1),
         // so this GEMM's grid is pending before the TC GEMM's and, launched on
@@ -284,7 +287,6 @@ extern "C" int hf_gemm_simt(const float* A, const float* B, float* C, int M, int
             HF_CUDA_CHECK(hf::end_side_launch(side, st));
             hf::sgemm_128x128<<<tiles, 256, smem, st>>>(At, B, C, M, N, K, hf::sgemm_group());
         }
-        cudaFreeAsync(At, st);
     } else {
         dim3 grid((N + 15) / 16, (M + 15) / 16);
         hf::sgemm_generic<<<grid, 256, 0, st>>>(A, B, C, M, N, K);

@@ -953,10 +953,12 @@ extern "C" int hf_gemm_tc(const float* A, const float* B, float* C, int M, int N
     const int Kp = bf16 ? (K + 7) / 8 * 8 : K;
     const int Ke = split ? 3 * Kp : K;
     const size_t elem = bf16 ? 2 : 4;
-    void* Bt = nullptr;
-    void* A3 = nullptr;
-    HF_CUDA_CHECK(cudaMallocAsync(&Bt, static_cast<size_t>(N) * Ke * elem, st));
-    HF_CUDA_CHECK(cudaMallocAsync(&A3, static_cast<size_t>(M) * Ke * elem, st));
+    void* Bt = hf::stream_scratch(device, st, 0, static_cast<size_t>(N) * Ke * elem);
+    void* A3 = hf::stream_scratch(device, st, 1, static_cast<size_t>(M) * Ke * elem);
+    if (!Bt || !A3) {
+        hf::set_error("hf_gemm_tc: cannot allocate %zu bytes of operand scratch", static_cast<size_t>(M + N) * Ke * elem);
+        return HF_ECUDA;
+    }
     // Co-scheduled with a SIMT replica: the pre-pass runs on a high-priority
     // side stream (level 1: one below the SIMT pre-pass), so its CTAs are
     // dispatched ahead of the SIMT GEMM's pending CTAs, while the GEMM itself
@@ -982,9 +984,6 @@ extern "C" int hf_gemm_tc(const float* A, const float* B, float* C, int M, int N
         hf::tc::round_a<<<pre_grid, 256, 0, ps>>>(reinterpret_cast<const float4*>(A), static_cast<float4*>(A3), n4);
     }
     HF_CUDA_CHECK(hf::end_side_launch(side, st));
-    int rc = bf16 ? hf::tc::launch<true>(A3, Bt, C, M, N, Ke, device, st, cosched)
-                  : hf::tc::launch<false>(A3, Bt, C, M, N, Ke, device, st, cosched);
-    cudaFreeAsync(Bt, st);
-    cudaFreeAsync(A3, st);
-    return rc;
+    return bf16 ? hf::tc::launch<true>(A3, Bt, C, M, N, Ke, device, st, cosched)
+                : hf::tc::launch<false>(A3, Bt, C, M, N, Ke, device, st, cosched);
 }
