@@ -519,3 +519,14 @@ def test_overwrite_area_skips_zero_fill_only_when_declared():
     m.request(a, "host", "w", protect=False)
     m.request(a, "host", "w", protect=False, zero_fill=False)
     assert calls == [True, False]
+
+
+def test_overwrite_flag_reaches_the_bound_task():
+    rt = hf.Runtime(hf.load_fleet(three_units()), backend=HostBackend())
+    t = rt.declare_task("t", (hf.Param.area("x", "r"), hf.Param.area("y", "w", overwrites=True),
+                              hf.Param.scalar("count")))
+    rt.attach_kernel(t, "k", "cpu", lambda ctx: None)
+    bound, _ = rt._bind(t, {"x": rt.register_data(bytes(16), 4, hf.ValueType.FLOAT32, "r"),
+                            "y": rt.register_data(bytes(16), 4, hf.ValueType.FLOAT32, "w"), "count": 4},
+                        None, None)
+    assert [p.overwrites for p in bound.params] == [False, True, False]
