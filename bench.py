@@ -587,6 +587,7 @@ def kernel_rooflines(device, n, kernels, torch):
     out = {}
 
     def time_it(fn, iters=10):
+        torch.cuda.synchronize()   # operands come from default-stream torch ops: finished before timing
         with torch.cuda.stream(st):
             for _ in range(3):
                 fn()

@@ -17,6 +17,7 @@ from paper_1405_2912_b200 import kernels  # noqa: E402
 
 
 def timed(fn, st, iters):
+    torch.cuda.synchronize()     # replicas were generated on the default stream
     with torch.cuda.stream(st):
         for _ in range(3):
             fn()
