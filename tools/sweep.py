@@ -17,6 +17,9 @@ from paper_1405_2912_b200 import kernels  # noqa: E402
 
 
 def timed(fn, st, iters):
+    """Device time per call over a Python launch loop.  Below ~16 MiB per
+    replica a vote_async call (~15 us of host time) outlasts the kernel, so
+    those rows are launch-bound, not kernel-bound."""
     torch.cuda.synchronize()     # replicas were generated on the default stream
     with torch.cuda.stream(st):
         for _ in range(3):
