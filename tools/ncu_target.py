@@ -18,7 +18,9 @@ c = torch.empty(n, n, device=d)
 dst = torch.empty_like(base)
 for _ in range(3):
     kernels.gemm_simt(a, b, c)
-    kernels.gemm_tc(a, b, c)
+    kernels.gemm_tc(a, b, c)                 # CTA-pair tf32
+    kernels.gemm_tc(a, b, c, mode=2)         # CTA-pair 3xBF16 (kind::f16)
+    kernels.gemm_tc(a, b, c, mode=0x100)     # single-CTA co-scheduling shape, tf32
     kernels.vote(reps[:2], 1e-3)
     kernels.vote(reps, 1e-3, voted=reps[0])
     kernels.checkpoint(dst, base)
