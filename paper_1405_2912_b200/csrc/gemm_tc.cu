@@ -734,45 +734,63 @@ __device__ __forceinline__ void bf16_split(float x, __nv_bfloat16& hi, __nv_bflo
     lo = __float2bfloat16_rn(x - __bfloat162float(hi));
 }
 
+// One thread per 8 consecutive k of a row: two 16-byte loads, three
+// 16-byte stores (hi | hi | lo segments).  Kp % 8 == 0 and K % 4 == 0, so a
+// vector is either fully inside K, half inside (K % 8 == 4), or padding.
 __global__ void __launch_bounds__(256) split3_a_bf16(const float* __restrict__ A, __nv_bfloat16* __restrict__ A3,
                                                      int M, int K, int Kp) {
-    const long long total = static_cast<long long>(M) * Kp;
-    const __nv_bfloat16 z = __float2bfloat16_rn(0.f);
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-         i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const long long m = i / Kp;
-        const int k = static_cast<int>(i % Kp);
-        __nv_bfloat16 hi = z, lo = z;
-        if (k < K) bf16_split(A[m * K + k], hi, lo);
-        __nv_bfloat16* row = A3 + m * 3LL * Kp;
-        row[k] = hi;
-        row[Kp + k] = hi;
-        row[2LL * Kp + k] = lo;
+    const int vpr = Kp / 8;                                   // vectors per row
+    const long long total = static_cast<long long>(M) * vpr;
+    for (long long v = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; v < total;
+         v += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long m = v / vpr;
+        const int k = static_cast<int>(v - m * vpr) * 8;
+        const float* src = A + m * K + k;
+        float x[8];
+        const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 x0 = k < K ? *reinterpret_cast<const float4*>(src) : z4;
+        const float4 x1 = k + 4 < K ? *reinterpret_cast<const float4*>(src + 4) : z4;
+        x[0] = x0.x, x[1] = x0.y, x[2] = x0.z, x[3] = x0.w, x[4] = x1.x, x[5] = x1.y, x[6] = x1.z, x[7] = x1.w;
+        __align__(16) __nv_bfloat16 hi[8], lo[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) bf16_split(x[q], hi[q], lo[q]);
+        uint4* row = reinterpret_cast<uint4*>(A3 + m * 3LL * Kp + k);
+        const uint4 h = *reinterpret_cast<const uint4*>(hi), l = *reinterpret_cast<const uint4*>(lo);
+        const long long seg = Kp / 8;                             // uint4 per segment
+        row[0] = h;
+        row[seg] = h;
+        row[2 * seg] = l;
     }
 }
 
+// 64(k) x 32(n) tiles: each thread stores bf16 pairs (two consecutive k), so
+// a warp writes 128 contiguous bytes of each output row segment.
 __global__ void __launch_bounds__(256) transpose_b_split3_bf16(const float* __restrict__ B,
                                                                __nv_bfloat16* __restrict__ Bt3, int K, int N,
                                                                int Kp) {
-    __shared__ float tile[32][33];
-    const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
+    __shared__ float tile[64][33];
+    const int k0 = blockIdx.y * 64, n0 = blockIdx.x * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
 #pragma unroll
-    for (int r = ty; r < 32; r += 8) {
+    for (int r = ty; r < 64; r += 8) {
         const int k = k0 + r, n = n0 + tx;
         tile[r][tx] = (k < K && n < N) ? B[static_cast<long long>(k) * N + n] : 0.f;
     }
     __syncthreads();
+    const int k = k0 + 2 * tx;                   // this thread's k pair
 #pragma unroll
     for (int r = ty; r < 32; r += 8) {
-        const int n = n0 + r, k = k0 + tx;
-        if (n < N && k < Kp) {
-            __nv_bfloat16 hi, lo;
-            bf16_split(tile[tx][r], hi, lo);       // zero (k >= K) splits to zeros
-            __nv_bfloat16* row = Bt3 + static_cast<long long>(n) * 3 * Kp;
-            row[k] = hi;
-            row[Kp + k] = lo;
-            row[2LL * Kp + k] = hi;
+        const int n = n0 + r;
+        if (n < N && k < Kp) {                   // Kp even: k + 1 < Kp too
+            __nv_bfloat16 h0, l0, h1, l1;        // zero (k >= K) splits to zeros
+            bf16_split(tile[2 * tx][r], h0, l0);
+            bf16_split(tile[2 * tx + 1][r], h1, l1);
+            __nv_bfloat162* row = reinterpret_cast<__nv_bfloat162*>(Bt3 + static_cast<long long>(n) * 3 * Kp + k);
+            const long long seg = Kp / 2;         // bf16 pairs per segment
+            const __nv_bfloat162 hh = __halves2bfloat162(h0, h1), ll = __halves2bfloat162(l0, l1);
+            row[0] = hh;
+            row[seg] = ll;
+            row[2 * seg] = hh;
         }
     }
 }
@@ -970,7 +988,7 @@ extern "C" int hf_gemm_tc(const float* A, const float* B, float* C, int M, int N
     HF_CUDA_CHECK(hf::begin_side_launch(side, st, &ps));
     const int pre_grid = hf::num_sms(device) * 8;
     if (bf16) {
-        dim3 tgrid((N + 31) / 32, (Kp + 31) / 32);
+        dim3 tgrid((N + 31) / 32, (Kp + 63) / 64);
         hf::tc::transpose_b_split3_bf16<<<tgrid, 256, 0, ps>>>(B, static_cast<__nv_bfloat16*>(Bt), K, N, Kp);
         hf::tc::split3_a_bf16<<<pre_grid, 256, 0, ps>>>(A, static_cast<__nv_bfloat16*>(A3), M, K, Kp);
     } else if (split) {
