@@ -707,18 +707,24 @@ __global__ void __launch_bounds__(256) round_a(const float4* __restrict__ A, flo
     }
 }
 
-__global__ void split3_a(const float* __restrict__ A, float* __restrict__ A3, int M, int K) {
-    long long total = static_cast<long long>(M) * K;
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-         i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        long long m = i / K, k = i % K;
-        float x = A[i];
-        float hi = to_tf32(x);
-        float lo = to_tf32(x - hi);
-        float* row = A3 + m * 3LL * K;
-        row[k] = hi;
-        row[K + k] = hi;
-        row[2LL * K + k] = lo;
+// One thread per 4 consecutive k (K % 4 == 0): one 16-byte load, three
+// 16-byte stores into the [A_hi | A_hi | A_lo] row.
+__global__ void __launch_bounds__(256) split3_a(const float* __restrict__ A, float* __restrict__ A3, int M, int K) {
+    const int vpr = K / 4;
+    const long long total = static_cast<long long>(M) * vpr;
+    for (long long v = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; v < total;
+         v += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long m = v / vpr;
+        const int k = static_cast<int>(v - m * vpr) * 4;
+        const float4 x = *reinterpret_cast<const float4*>(A + m * K + k);
+        const float4 hi = make_float4(to_tf32(x.x), to_tf32(x.y), to_tf32(x.z), to_tf32(x.w));
+        const float4 lo = make_float4(to_tf32(x.x - hi.x), to_tf32(x.y - hi.y), to_tf32(x.z - hi.z),
+                                      to_tf32(x.w - hi.w));
+        float4* row = reinterpret_cast<float4*>(A3 + m * 3LL * K + k);
+        const long long seg = K / 4;
+        row[0] = hi;
+        row[seg] = hi;
+        row[2 * seg] = lo;
     }
 }
 
