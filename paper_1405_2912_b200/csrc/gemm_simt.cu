@@ -225,6 +225,11 @@ static int sgemm_cosched_smem() {
 // Tile-row group of the grouped CTA order (HF_SGEMM_GROUP, default 16: at
 // 4096^3 the resident CTAs then share 16 A panels and ~19 B panels in L2;
 // DRAM reads 333 MB with 8, 286 MB with 16, 509 MB with 32, same time).
+static bool side_prepass() {
+    static const int on = getenv("HF_SIMT_SIDE_PREPASS") == nullptr || getenv("HF_SIMT_SIDE_PREPASS")[0] != '0';
+    return on != 0;
+}
+
 static bool simt_pdl() {
     static const int on = getenv("HF_SIMT_PDL") != nullptr && getenv("HF_SIMT_PDL")[0] == '1';
     return on != 0 && pdl_enabled();
@@ -279,12 +284,24 @@ extern "C" int hf_gemm_simt(const float* A, const float* B, float* C, int M, int
             HF_CUDA_CHECK(hf::launch_pdl(hf::transpose_a, dim3(K / 32, M / 32), dim3(256), 0, st, A, At, M, K));
             HF_CUDA_CHECK(hf::launch_pdl(hf::sgemm_128x128, dim3(tiles), dim3(256), smem, st, At, B, C, M, N, K,
                                          hf::sgemm_group()));
-        } else {
+        } else if (hf::side_prepass()) {
+            // default: the pre-pass on the device's greatest-priority side
+            // stream, joined back by an event (~20 us of launch gap before
+            // the GEMM, but the A^T pass reliably finishes before the TC
+            // replica's pre-pass, so the SIMT grid is pending first)
             hf::SideStream* side = (mode & HF_GEMM_COSCHEDULE) ? hf::side_stream(device, 0) : nullptr;
             cudaStream_t ps = st;
             HF_CUDA_CHECK(hf::begin_side_launch(side, st, &ps));
             hf::transpose_a<<<dim3(K / 32, M / 32), 256, 0, ps>>>(A, At, M, K);
             HF_CUDA_CHECK(hf::end_side_launch(side, st));
+            hf::sgemm_128x128<<<tiles, 256, smem, st>>>(At, B, C, M, N, K, hf::sgemm_group());
+        } else {
+            // HF_SIMT_SIDE_PREPASS=0: pre-pass and GEMM in stream order on the
+            // caller's stream (no event gap).  Co-scheduled, the TC pre-pass
+            // then often finished first and its GEMM took the SMs ahead of
+            // the SIMT grid, even with the lead stream at the greatest priority
+            // (2.44 -> 2.57 ms per DMR round)
+            hf::transpose_a<<<dim3(K / 32, M / 32), 256, 0, st>>>(A, At, M, K);
             hf::sgemm_128x128<<<tiles, 256, smem, st>>>(At, B, C, M, N, K, hf::sgemm_group());
         }
     } else {
