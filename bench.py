@@ -427,8 +427,9 @@ def run_hetft_arm(args, rank, world, local):
 
     # ---- kernel-level measurements (same process, after the timed regions) ----
     kern = kernel_rooflines(device, n, kernels, torch)
-    tmr = tmr_rate(device, n, args.fault_prob, args.seed + 7919 * rank, args.steps, args.warmup, torch) \
-        if not args.no_tmr else None
+    # at least 30 timed tasks: a 20-task window swings with the fault draws
+    tmr = tmr_rate(device, n, args.fault_prob, args.seed + 7919 * rank, max(30, args.steps),
+                   max(5, args.warmup), torch) if not args.no_tmr else None
     detect = detect_rate(device, n, kernels, torch, args.seed, probes=args.detect_probes) if rank == 0 else None
 
     total_tasks = args.steps * world
