@@ -451,3 +451,31 @@ def test_vector_workloads_match_numpy(K, n):
     exp = np.full(n, 7.0, np.float32)
     exp[:n - 1] = a[:n - 1] + np.float32(1.0)
     assert out2.cpu().numpy().tobytes() == exp.tobytes()
+
+
+def test_launches_capture_in_a_cuda_graph(K):
+    """libhetft launches (PDL attributes included) can be captured in a CUDA
+    graph and replayed: the replayed vote sees a changed replica and the
+    replayed checkpoint copies the current bytes."""
+    n = (1 << 20) + 5
+    st = torch.cuda.Stream()
+    a = torch.rand(n, device="cuda") + 1
+    b = a.clone()
+    dst = torch.empty_like(a)
+    ws = K.VoteWorkspace(0, stream=st)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        K.vote_async([a, b], ws, 1e-3, stream=st)
+        K.checkpoint(dst, a, stream=st)
+    g.replay()
+    torch.cuda.synchronize()
+    assert ws.read().verdict == "match"
+    assert torch.equal(dst, a)
+    b[777] += 1.0
+    a[5] = 3.5
+    g.replay()
+    torch.cuda.synchronize()
+    r = ws.read()
+    assert (r.verdict, r.first_div, r.mismatch) == ("mismatch", 5, [2, 2])
+    assert torch.equal(dst, a)

@@ -368,3 +368,25 @@ def test_c1_tmr_1024_single_seeded_bitflip(seed):
         assert rep.votes == ["match"]
     got = rt.read_array(ic)
     assert ovote.reference_first_divergence(got, omatmul.matmul(a, b).reshape(-1), 1e-3) is None
+
+
+@pytest.mark.gpu
+def test_reserve_presizes_the_device_heap():
+    """Runtime.reserve(space, nbytes, count): the caching allocator then holds
+    count free blocks, so count buffers of that size for the space's compute
+    stream allocate no new device segment (no cudaMalloc inside a stream)."""
+    cfg = hf.gpu_fleet_config(devices=(0,), kinds=("gpu-tc", "gpu-simt"))
+    rt = hf.Runtime(hf.load_fleet(cfg))
+    nb = 48 << 20
+    torch.cuda.synchronize()
+    reserved0 = torch.cuda.memory_stats().get("reserved_bytes.all.current", 0)
+    rt.reserve("gpu0mem", nb, 6)
+    stats = torch.cuda.memory_stats()
+    assert stats.get("reserved_bytes.all.current", 0) >= reserved0 + 6 * nb
+    seg0 = stats.get("segment.all.allocated", 0)
+    sp = rt.fleet.spaces["gpu0mem"]
+    bufs = [rt.backend.alloc(sp, nb, zero=False) for _ in range(6)]
+    assert torch.cuda.memory_stats().get("segment.all.allocated", 0) == seg0
+    del bufs
+    with pytest.raises(hf.UnknownSpaceError):
+        rt.reserve("nowhere", nb, 1)
