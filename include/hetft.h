@@ -108,8 +108,10 @@ int hf_vote(const void* const* replicas, int K, int64_t n, int dtype,
             const double* rel_tol, const int32_t* ulp_tol,
             void* voted, hf_vote_result* out, int device, void* stream);
 
-/* Asynchronous variant: writes the result to `dev_out` (device memory) and
- * returns without synchronising.  `workspace` is caller-owned device memory
+/* Asynchronous variant: writes the result to `dev_out` and returns without
+ * synchronising.  `dev_out` may be device memory or pinned host memory
+ * (device-visible through UVA): then the last CTA stores the 96-byte result
+ * straight over the bus and no separate read-back copy is needed.  `workspace` is caller-owned device memory
  * of hf_vote_workspace_bytes() bytes initialised once with
  * hf_vote_workspace_init(); the kernel leaves it re-initialised, so one
  * workspace serves any number of back-to-back votes on one stream. */

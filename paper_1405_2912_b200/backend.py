@@ -349,9 +349,11 @@ class CudaBackend:
         slot = self._vote_slot(device)
         start = self.timer_start(st, device)
         dt = torch_dtype(view_dtype(value_type, width))
+        # the kernel's last CTA writes the result straight into the slot's
+        # pinned host buffer (UVA): no separate 96-byte read-back copy
         kernels.vote_async([b.view(dt) for b in bufs], slot.ws, rel_tol, ulp_tol,
-                           voted=voted.view(dt) if voted is not None else None, stream=st)
-        kernels.copy(slot.host, slot.ws.result, stream=st)
+                           voted=voted.view(dt) if voted is not None else None, stream=st,
+                           result_into=slot.host)
         stop = self.timer_stop(start, st, device)
         self.launches += 1
         return _PendingVote(self, slot, device, stop)
@@ -447,7 +449,7 @@ class _PendingVote:
         self.ready = getattr(stop, "stop_event", None)   # after the vote kernel (voted bytes final)
 
     def wait(self):
-        ns = self._stop()            # synchronises the stop event (after the D2H)
+        ns = self._stop()            # synchronises the stop event (after the vote kernel)
         raw = self._slot.host.numpy().tobytes()
         self._be._release_vote_slot(self._dev, self._slot)
         return kernels.VoteResult.from_c(_lib.HfVoteResult.from_buffer_copy(raw)), ns

@@ -176,13 +176,17 @@ class VoteWorkspace:
 
 def vote_async(replicas: Sequence[torch.Tensor], ws: VoteWorkspace, rel_tol=0.001, ulp_tol=None,
                voted: Optional[torch.Tensor] = None,
-               stream: Optional[torch.cuda.Stream] = None) -> None:
+               stream: Optional[torch.cuda.Stream] = None,
+               result_into: Optional[torch.Tensor] = None) -> None:
+    """result_into: a pinned host buffer of sizeof(HfVoteResult) bytes that
+    receives the result directly (default: ws.result in device memory)."""
     K = len(replicas)
     n = replicas[0].numel()
     rel_c, ulp_c = _tolerances(K, rel_tol, ulp_tol)
+    out = ws.result if result_into is None else result_into
     rc = _lib.load().hf_vote_async(_ptr_array(replicas), K, n, hf_dtype(replicas[0]), rel_c, ulp_c,
                                    voted.data_ptr() if voted is not None else None,
-                                   ws.result.data_ptr(), ws.ws.data_ptr(), ws.device,
+                                   out.data_ptr(), ws.ws.data_ptr(), ws.device,
                                    _stream_ptr(ws.device, stream))
     check("hf_vote_async", rc)
     _count()
@@ -232,8 +236,7 @@ def vote_sliced(replicas: Sequence[torch.Tensor], rel_tol=0.001, ulp_tol=None,
             slot = _SLICE_SLOTS[(d, i)] = _SliceSlot(d)
         views = [r[lo:hi] for r in replicas]
         vote_async(views, slot.ws, rel_tol, ulp_tol, voted=voted[lo:hi] if voted is not None else None,
-                   stream=st)
-        copy(slot.host, slot.ws.result, stream=st)
+                   stream=st, result_into=slot.host)
         ev = torch.cuda.Event()
         ev.record(st)
         pending.append((lo, slot, ev))
