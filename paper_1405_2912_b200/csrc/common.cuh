@@ -42,7 +42,10 @@ SideStream* side_stream(int device, int level);
 // later call on the same stream (stream order makes reuse safe), grown with
 // cudaMallocAsync/cudaFreeAsync on that stream when a call needs more.  Saves
 // the per-call allocate/free pair of the GEMM pre-passes.  Never freed (the
-// process owns a few per unit stream).  Returns nullptr on failure.
+// process owns a few per unit stream).  Returns nullptr on failure.  Calls
+// that share a stream must come from one host thread at a time (the runtime
+// launches each unit stream from its dispatcher thread), since a growth frees
+// the old block in stream order.
 void* stream_scratch(int device, cudaStream_t st, int slot, size_t bytes);
 // begin: lock + fork, *launch_stream = side stream (or `st` when side is
 // NULL).  end: check the launches, join back into `st`, unlock.  Both return
