@@ -75,3 +75,24 @@ def test_tmr_single_fault_corrected():
     assert res.mismatch == [0, 1, 0]
     assert res.first_div == 17 and res.winner == 0
     assert np.array_equal(res.voted, x)
+
+
+@pytest.mark.parametrize("row", inject_golden()["attempts"])
+def test_simulate_execution_replays_reference(row):
+    """The drop-in's simulate_execution (reference devices.py:223-259 API over
+    host numpy views) reproduces the reference's recorded outcomes: fault
+    class, corrupted element and the bytes of every write view."""
+    import paper_1405_2912_b200 as hf
+    dt = _DT[row["kind"]]
+    vt = hf.ValueType.FLOAT32 if row["kind"] == "f32" else hf.ValueType.FLOAT64 if row["kind"] == "f64" \
+        else hf.ValueType.INT
+    views = [np.frombuffer(bytes.fromhex(h), dtype=dt).copy() for h in row["before"]]
+    unit = {"id": "u", "kind": "cpu", "memory_space": "host", "seed": row["seed"],
+            "corrupt_rel_magnitude": row["rel"], "corrupt_element": row["element"]}
+    unit.update(dict(zip(("abort_prob", "api_error_prob", "hang_prob", "corrupt_prob"), row["probs"])))
+    fleet = hf.load_fleet({"memory_spaces": [{"id": "host", "host": True}], "units": [unit]})
+    out = hf.simulate_execution(fleet.units["u"], "k", "cpu", views[0].size, write_views=[(v, vt) for v in views])
+    assert (out.fault.value if out.fault is not None else None) == row["fault"]
+    if row["corrupted_index"] is not None:
+        assert out.corrupted_index == row["corrupted_index"]
+    assert [v.tobytes().hex() for v in views] == row["after"]
