@@ -68,10 +68,12 @@ class HostBackend:
         return False
 
     def alloc(self, space, nbytes, zero=True):
-        return np.zeros(nbytes, dtype=np.uint8) if zero else np.empty(nbytes, dtype=np.uint8)
+        return _HostBytes(nbytes)
 
     def from_bytes(self, space, data):
-        return np.frombuffer(bytes(data), dtype=np.uint8).copy()
+        buf = _HostBytes(len(data))
+        buf[:] = np.frombuffer(bytes(data), dtype=np.uint8)
+        return buf
 
     def to_bytes(self, buf):
         return buf.tobytes()
@@ -122,3 +124,16 @@ class HostBackend:
         if voted is not None:
             voted[:] = o.voted.view(np.uint8)
         return _VoteResult(o), time.perf_counter_ns() - t0
+
+
+class _HostBytes(np.ndarray):
+    """uint8 host payload that also accepts bytes-like slice assignment, as
+    the reference's bytearray payloads do (h.payload[:] = b"...")."""
+
+    def __new__(cls, nbytes):
+        return np.zeros(nbytes, dtype=np.uint8).view(cls)
+
+    def __setitem__(self, key, value):
+        if isinstance(value, (bytes, bytearray, memoryview)):
+            value = np.frombuffer(bytes(value), dtype=np.uint8)
+        super().__setitem__(key, value)
