@@ -516,7 +516,7 @@ def fp32_peak(sm_max_mhz: float):
 def ncu_traffic(*kernels_):
     """DRAM bytes per launch of `kernels_` summed, from the newest committed
     ncu --set full capture summary (tools/ncu_traffic.py), or None."""
-    for p in sorted((ROOT / "profiles").glob("r*_ncu_traffic.json"), reverse=True):
+    for p in sorted((ROOT / "profiles").glob("r*_ncu_traffic*.json"), reverse=True):
         ks = json.loads(p.read_text())["kernels"]
         if all(k in ks for k in kernels_):
             return sum(ks[k]["traffic_bytes"] for k in kernels_)
