@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--n", type=int, default=4096)
     ap.add_argument("--fault-prob", type=float, default=0.05, help="per-replica corrupt (bit flip) probability")
     ap.add_argument("--seed", type=int, default=1)
-    ap.add_argument("--e2e-steps", type=int, default=None, help="default max(40, --steps)")
+    ap.add_argument("--e2e-steps", type=int, default=None, help="default max(80, --steps)")
     ap.add_argument("--depth", type=int, default=1, help="TaskStream depth (tasks in flight beyond the one settling)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tmr", action="store_true", help="skip the HetTMR 4096^2 side measurement")
@@ -361,9 +361,9 @@ def run_hetft_arm(args, rank, world, local):
     t_max = max_over_ranks(t_dev)
 
     # ---- e2e: host buffers through the same API (H2D inside invoke, D2H read) ----
-    # at least 40 steps: the pipeline fill (first 128 MiB H2D before any
+    # at least 80 steps: the pipeline fill (first 128 MiB H2D before any
     # kernel can start) and drain (last D2H) are paid once per timed region
-    e2e_steps = args.e2e_steps or max(40, args.steps)
+    e2e_steps = args.e2e_steps or max(80, args.steps)
     hA = torch.empty(nb, dtype=torch.uint8).pin_memory()
     hB = torch.empty(nb, dtype=torch.uint8).pin_memory()
     hC = torch.empty(nb, dtype=torch.uint8).pin_memory()
