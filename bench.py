@@ -390,12 +390,14 @@ def run_hetft_arm(args, rank, world, local):
         # busy while the host blocks on a re-dispatched (mismatching) task
         staged = [stage(i) for i in range(min(LOOKAHEAD, steps))]
         queue, retired, last = [], [], None
+        reps = []
         with rt.task_stream(depth=args.depth) as ts:
             for i in range(steps):
                 ia, ib, ic = staged.pop(0)
                 if i + LOOKAHEAD < steps:
                     staged.append(stage(i + LOOKAHEAD))
                 queue.append((ts.submit(task, {"A": ia, "B": ib, "C": ic, "n": n}, strat), (ia, ib, ic)))
+                reps.append(queue[-1][0])
                 if args.trace_steps:
                     print(f"e2e step {i} t={time.perf_counter():.6f} rounds={queue[-1][0].rounds}", file=sys.stderr)
                 while queue and queue[0][0].success:
@@ -411,13 +413,14 @@ def run_hetft_arm(args, rank, world, local):
             last.synchronize()
         for x in retired:
             rt.release(x)
+        return sum(r.rounds for r in reps)
 
     host_stream(2)
     torch.cuda.synchronize()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    host_stream(e2e_steps)
+    e2e_rounds = host_stream(e2e_steps)
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -469,6 +472,9 @@ def run_hetft_arm(args, rank, world, local):
                    "strategy": "hetdmr", "parallelism": f"independent task streams x{world}",
                    "l2": "operands (3 x 64 MiB) exceed the 126 MB L2; no flush needed"},
         "e2e": {"value": (e2e_steps * world) / t_e2e, "unit": "tasks/s", "steps": e2e_steps,
+                "rounds": e2e_rounds,
+                "note": "own window of max(80, steps) tasks with their own fault draws; the H2D of "
+                        "step i+2 and the D2H of step i-1 overlap step i, PCIe-bound (~2.56 ms/step)",
                 "h2d_bytes_per_step": 2 * nb,
                 "d2h_bytes_per_step": nb},
         "gpu_launches": launches,
