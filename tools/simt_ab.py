@@ -1,5 +1,9 @@
 """A/B the SIMT launch with and without the k-split tail wave
-(HF_SIMT_NO_TAIL_SPLIT is read once per process: one subprocess each)."""
+(HF_SIMT_NO_TAIL_SPLIT is read once per process: one subprocess each).
+
+Historical: the k-split tail was measured slower and reverted (DESIGN.md §4,
+"Tried and reverted"), so both arms now run the same kernel; kept as the
+record of how that A/B was taken."""
 import json
 import os
 import subprocess

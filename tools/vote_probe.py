@@ -1,5 +1,8 @@
 """Why are diverse-replica votes slower than identical-replica votes at
->= 1 GiB (profiles/r01_vote_sweep_v2.json)?  Times hf_vote K = 3 / 5 on
+>= 1 GiB (profiles/r01_vote_sweep_v2.json)?  Answer (later): they are not —
+the sweep timed the votes while the default-stream torch ops generating the
+diverse replicas were still running; with a device synchronise first both
+kinds run at 1.08-1.14 of the HBM copy peak (profiles/r01_sweep_v4_*.json).  Times hf_vote K = 3 / 5 on
 1 GiB replicas built several ways and prints their base addresses, so value
 effects (which screen path runs) separate from placement effects."""
 import json
