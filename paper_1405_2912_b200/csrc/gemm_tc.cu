@@ -36,11 +36,9 @@ constexpr int BM = 128;
 constexpr int BN = 256;
 constexpr int BK = 32;          // one 128-byte swizzle row of fp32
 constexpr int A_STAGE = BM * BK * 4;   // 16 KB
-constexpr int B_STAGE = BN * BK * 4;   // 32 KB
-constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
 constexpr int NUM_THREADS = 256;
-template <int S>
-constexpr int smem_bytes() { return S * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/; }
+template <int S, int BNT = BN>
+constexpr int smem_bytes() { return S * (A_STAGE + BNT * BK * 4) + 1024 /*align*/ + 256 /*barriers*/; }
 
 // ---- PTX wrappers ----------------------------------------------------------
 
@@ -186,22 +184,23 @@ struct Barriers {
 // overlaps a tile's epilogue with the next tile's main loop; 1: one tile per
 // CTA, 2 CTAs/SM co-resident, used when the kernel shares the GPU with the
 // SIMT replica so its CTAs fill the SIMT kernel's last wave).
-template <int STAGES, int ACCS, bool BF16 = false>
+template <int STAGES, int ACCS, bool BF16 = false, int BNT = BN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, float* __restrict__ C,
                  int M, int N, int K) {
     using OK = OpKind<BF16>;
+    constexpr int SB = A_STAGE + BNT * BK * 4;      // bytes per stage (B tile BNT rows of 128 B)
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment for the SWIZZLE_128B atoms
     const uint32_t base_u32 = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + ((1024 - (base_u32 & 1023)) & 1023);
-    constexpr int TMEM_COLS = ACCS * BN;
-    Barriers<STAGES>* bars = reinterpret_cast<Barriers<STAGES>*>(smem + STAGES * STAGE_BYTES);
+    constexpr int TMEM_COLS = ACCS * BNT;
+    Barriers<STAGES>* bars = reinterpret_cast<Barriers<STAGES>*>(smem + STAGES * SB);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int tiles_m = (M + BM - 1) / BM;
-    const int tiles_n = (N + BN - 1) / BN;
+    const int tiles_n = (N + BNT - 1) / BNT;
     const int num_tiles = tiles_m * tiles_n;
     const int nkb = (K + OK::BKE - 1) / OK::BKE;
 
@@ -236,12 +235,12 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
                 const int tm = tile % tiles_m, tn = tile / tiles_m;
-                const int m0 = tm * BM, n0 = tn * BN;
+                const int m0 = tm * BM, n0 = tn * BNT;
                 for (int kb = 0; kb < nkb; ++kb) {
                     mbar_wait(&bars->empty[stage], phase ^ 1);
-                    uint8_t* sa = smem + stage * STAGE_BYTES;
+                    uint8_t* sa = smem + stage * SB;
                     uint8_t* sb = sa + A_STAGE;
-                    mbar_expect_tx(&bars->full[stage], STAGE_BYTES);
+                    mbar_expect_tx(&bars->full[stage], SB);
                     tma_load_2d(sa, &tmA, &bars->full[stage], kb * OK::BKE, m0);
                     tma_load_2d(sb, &tmB, &bars->full[stage], kb * OK::BKE, n0);
                     if (++stage == STAGES) {
@@ -254,7 +253,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     } else if (warp == 1) {
         // ===== MMA issuer =====
         if (lane == 0) {
-            constexpr uint32_t idesc = make_idesc(BM, BN, OK::FMT);
+            constexpr uint32_t idesc = make_idesc(BM, BNT, OK::FMT);
             int stage = 0;
             uint32_t phase = 0;
             int local = 0;
@@ -263,11 +262,11 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 const uint32_t acc_phase = (local / ACCS) & 1;
                 mbar_wait(&bars->tmem_empty[acc], acc_phase ^ 1);
                 tc_fence_after();
-                const uint32_t d_tmem = tmem + acc * BN;
+                const uint32_t d_tmem = tmem + acc * BNT;
                 for (int kb = 0; kb < nkb; ++kb) {
                     mbar_wait(&bars->full[stage], phase);
                     tc_fence_after();
-                    const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+                    const uint32_t sa = smem_u32(smem + stage * SB);
                     const uint32_t sb = sa + A_STAGE;
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {   // 4 UMMAs of 32 bytes of K per 128-byte row
@@ -293,15 +292,15 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         int local = 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
             const int tm = tile % tiles_m, tn = tile / tiles_m;
-            const int m0 = tm * BM, n0 = tn * BN;
+            const int m0 = tm * BM, n0 = tn * BNT;
             const int acc = local % ACCS;
             mbar_wait(&bars->tmem_full[acc], (local / ACCS) & 1);
             tc_fence_after();
             const int row = m0 + row_in_tile;
-            const uint32_t tbase = tmem + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
+            const uint32_t tbase = tmem + (static_cast<uint32_t>(ew * 32) << 16) + acc * BNT;
             float* crow = C + static_cast<long long>(row) * N;
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
+            for (int c = 0; c < BNT / 32; ++c) {
                 float v[32];
                 tmem_ld32(tbase + c * 32, v);
                 const int col0 = n0 + c * 32;
@@ -846,6 +845,7 @@ constexpr int PAIR_STAGES = 6;
 
 static const int kRegistered = register_kernels(
     {(const void*)gemm_tf32_kernel<4, 2>, (const void*)gemm_tf32_kernel<2, 1>,
+     (const void*)gemm_tf32_kernel<3, 1, false, 128>, (const void*)gemm_tf32_kernel<3, 1, true, 128>,
      (const void*)gemm_tf32_pair_kernel<PAIR_STAGES>, (const void*)gemm_tf32_kernel<4, 2, true>,
      (const void*)gemm_tf32_kernel<2, 1, true>, (const void*)gemm_tf32_pair_kernel<PAIR_STAGES, true>,
      (const void*)transpose_b<true>, (const void*)transpose_b<false>, (const void*)round_a, (const void*)split3_a,
@@ -870,6 +870,17 @@ static bool split_enabled() {
         on = (e && e[0] == '0') ? 0 : 1;
     }
     return on == 1;
+}
+
+// Co-scheduled tile width: HF_TC_COSCHED_BN=128 (3 stages of 128 x 128) or
+// 256 (2 stages of 128 x 256, the default).
+static int cosched_bn() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("HF_TC_COSCHED_BN");
+        v = (e && atoi(e) == 128) ? 128 : 256;
+    }
+    return v;
 }
 
 // Launch shape: CTA pairs (6 stages, double-buffered TMEM, 74 persistent
@@ -929,9 +940,11 @@ static int launch(const void* A, const void* Bt, float* C, int M, int N, int K, 
         HF_CHECK_LAUNCH();
         return HF_OK;
     }
+    const bool narrow = cosched && cosched_bn() == 128;
     int rc = make_map(&ta, A, static_cast<uint64_t>(K), static_cast<uint64_t>(M), pitch, OK::BKE, BM, BF16);
     if (rc) return rc;
-    rc = make_map(&tb, Bt, static_cast<uint64_t>(K), static_cast<uint64_t>(N), pitch, OK::BKE, BN, BF16);
+    rc = make_map(&tb, Bt, static_cast<uint64_t>(K), static_cast<uint64_t>(N), pitch, OK::BKE, narrow ? 128 : BN,
+                  BF16);
     if (rc) return rc;
     const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
     static bool attr_set[64] = {false};
@@ -940,9 +953,18 @@ static int launch(const void* A, const void* Bt, float* C, int M, int N, int K, 
                                            smem_bytes<4>()));
         HF_CUDA_CHECK(cudaFuncSetAttribute(gemm_tf32_kernel<2, 1, BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            smem_bytes<2>()));
+        HF_CUDA_CHECK(cudaFuncSetAttribute(gemm_tf32_kernel<3, 1, BF16, 128>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<3, 128>()));
         attr_set[device] = true;
     }
-    if (cosched) {
+    if (narrow) {
+        // co-scheduled, 128 x 128 tiles and 3 stages in about the smem of
+        // 2 stages of 128 x 256: twice the CTAs, each half as long, so they
+        // pack the SIMT grid's last wave more tightly
+        const int tiles_narrow = ((M + BM - 1) / BM) * ((N + 127) / 128);
+        gemm_tf32_kernel<3, 1, BF16, 128><<<tiles_narrow, NUM_THREADS, smem_bytes<3, 128>(), st>>>(ta, tb, C, M, N,
+                                                                                                K);
+    } else if (cosched) {
         gemm_tf32_kernel<2, 1, BF16><<<tiles, NUM_THREADS, smem_bytes<2>(), st>>>(ta, tb, C, M, N, K);
     } else {
         const int sms = num_sms(device);
