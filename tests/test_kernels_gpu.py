@@ -479,3 +479,42 @@ def test_launches_capture_in_a_cuda_graph(K):
     r = ws.read()
     assert (r.verdict, r.first_div, r.mismatch) == ("mismatch", 5, [2, 2])
     assert torch.equal(dst, a)
+
+
+def test_pdl_launch_matches_classic_launch(K):
+    """Programmatic dependent launch (default) and classic launches
+    (HF_PDL=0, read once per process, hence a child process) give bit-identical
+    votes, copies and vector-kernel outputs."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+from paper_1405_2912_b200 import kernels as K
+g = torch.Generator(device="cuda").manual_seed(11)
+n = (1 << 20) + 3
+a = torch.rand(n, device="cuda", generator=g) + 1
+reps = [a.clone() for _ in range(3)]
+K.inject_bitflip(reps[1], 77, 29)
+K.inject_bitflip(reps[2], 99, 30)
+voted = torch.empty_like(a)
+r = K.vote(reps, 1e-3, voted=voted)
+dst = torch.empty_like(a)
+K.checkpoint(dst, reps[1])
+inc = torch.empty_like(a)
+K.vec_path(a, inc)
+np.savez(sys.argv[1], voted=voted.cpu().numpy(), dst=dst.cpu().numpy(), inc=inc.cpu().numpy(),
+         res=np.array(r.mismatch + [r.unresolved, r.first_div, r.winner]))
+''' % root
+    with tempfile.TemporaryDirectory() as td:
+        outs = []
+        for pdl in ("1", "0"):
+            f = os.path.join(td, f"pdl{pdl}.npz")
+            subprocess.run([sys.executable, "-c", code, f], env=dict(os.environ, HF_PDL=pdl), check=True,
+                           timeout=120)
+            outs.append(np.load(f))
+        for key in ("voted", "dst", "inc", "res"):
+            assert outs[0][key].tobytes() == outs[1][key].tobytes(), key
