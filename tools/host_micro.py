@@ -1,3 +1,6 @@
+"""Host-side cost of the CudaBackend building blocks (allocation with and
+without a stream switch, fill, events, stream waits, views), microseconds
+per call; used to pick the host-path optimisations in DESIGN.md §4."""
 import time, torch, sys
 sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
 from paper_1405_2912_b200 import kernels
