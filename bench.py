@@ -510,8 +510,10 @@ def fp32_peak(sm_max_mhz: float):
             d = json.loads(out.stdout.strip().splitlines()[-1])
             if out.returncode != 0 or not d["ffma2_tflops"] > 0:
                 raise ValueError(d.get("error"))
-            return d["ffma2_tflops"], ("measured live: tools/fp32_peak (FFMA2 loop, 148x4 CTAs, best of 5); "
-                                       f"FFMA2 in the GEMM's broadcast operand form peaks at {d['ffma2_bcast_tflops']:.1f}")
+            return d["ffma2_tflops"], ("measured live: tools/fp32_peak (FFMA2 loop, 148x4 CTAs, best of 5; an 8x8 "
+                                       "outer product issued b-pair-outer reaches it too, tools/ffma2_forms.cu); "
+                                       f"issued a-scalar-outer it peaks at {d['ffma2_bcast_tflops']:.1f}, which is "
+                                       "where ptxas's schedule of the GEMM lands")
         except (OSError, ValueError, KeyError, IndexError, subprocess.SubprocessError):
             pass
     for p in sorted((ROOT / "profiles").glob("r*_fp32_peak.json"), reverse=True):
