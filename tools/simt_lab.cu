@@ -217,6 +217,125 @@ sgemm_diag(const float* __restrict__ At, const float* __restrict__ B, float* __r
     }
 }
 
+
+// 16 (m) x 4 (n) thread tile: per k-step 16 broadcast a scalars x 2 b pairs,
+// issued b-pair-outer so each b pair is reused by 16 consecutive FFMA2 (the
+// form tools/ffma2_forms.cu measured at the FFMA2 peak).  Warp = 32 lanes
+// along n (b fragment 512 contiguous bytes), 8 warps along m (a fragment
+// broadcast).  Each output is the same FMA chain in k order as the product
+// kernel, so results are bit-identical.
+template <int BK, int ST, bool B_OUTER>
+__global__ void __launch_bounds__(256, 2)
+sgemm_16x4(const float* __restrict__ At, const float* __restrict__ B, float* __restrict__ C, int M, int N, int K) {
+    constexpr int BM = 128, BN = 128;
+    extern __shared__ __align__(16) float sm[];
+    float* As = sm;
+    float* Bs = sm + ST * BK * BM;
+    const int t = threadIdx.x;
+    const int tx = t & 31;          // n: columns 4*tx .. 4*tx+3
+    const int ty = t >> 5;          // m: rows 16*ty .. 16*ty+15
+    const int tiles_n = N / BN, tiles_m = M / BM;
+    const int group = 16, bid = blockIdx.x, per_group = group * tiles_n;
+    const int g = bid / per_group, first_m = g * group;
+    const int gm = min(tiles_m - first_m, group);
+    const int tm = first_m + (bid % per_group) % gm, tn = (bid % per_group) / gm;
+    const int m0 = tm * BM, n0 = tn * BN;
+    const int c_row = t >> 5, c_col = (t & 31) * 4;
+    const float* Ag = At + static_cast<long long>(c_row) * M + m0 + c_col;
+    const float* Bg = B + static_cast<long long>(c_row) * N + n0 + c_col;
+    auto issue = [&](int kt, int stage) {
+        const long long ka = static_cast<long long>(kt) * BK * M;
+        const long long kb = static_cast<long long>(kt) * BK * N;
+        float* as = As + stage * BK * BM + c_row * BM + c_col;
+        float* bs = Bs + stage * BK * BN + c_row * BN + c_col;
+#pragma unroll
+        for (int r = 0; r < BK; r += 8) {
+            cp_async16(as + r * BM, Ag + ka + static_cast<long long>(r) * M);
+            cp_async16(bs + r * BN, Bg + kb + static_cast<long long>(r) * N);
+        }
+    };
+    unsigned long long acc[16][2];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = 0ull;
+    const int nk = K / BK;
+#pragma unroll
+    for (int s = 0; s < ST - 1; ++s) {
+        if (s < nk) issue(s, s);
+        cp_async_commit();
+    }
+    for (int kt = 0; kt < nk; ++kt) {
+        cp_async_wait<ST - 2>();
+        __syncthreads();
+        {
+            const int nt = kt + ST - 1;
+            if (nt < nk) issue(nt, nt % ST);
+            cp_async_commit();
+        }
+        const float* as = As + (kt % ST) * BK * BM + ty * 16;
+        const float* bs = Bs + (kt % ST) * BK * BN + tx * 4;
+#pragma unroll
+        for (int k = 0; k < BK; ++k) {
+            const float4 a0 = *reinterpret_cast<const float4*>(as + k * BM);
+            const float4 a1 = *reinterpret_cast<const float4*>(as + k * BM + 4);
+            const float4 a2 = *reinterpret_cast<const float4*>(as + k * BM + 8);
+            const float4 a3 = *reinterpret_cast<const float4*>(as + k * BM + 12);
+            const float4 bv = *reinterpret_cast<const float4*>(bs + k * BN);
+            const float a[16] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w,
+                                 a2.x, a2.y, a2.z, a2.w, a3.x, a3.y, a3.z, a3.w};
+            const unsigned long long b[2] = {pack2(bv.x, bv.y), pack2(bv.z, bv.w)};
+            if (B_OUTER) {
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) ffma2(acc[i][j], pack2(a[i], a[i]), b[j]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const unsigned long long ai = pack2(a[i], a[i]);
+                    ffma2(acc[i][0], ai, b[0]);
+                    ffma2(acc[i][1], ai, b[1]);
+                }
+            }
+        }
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        float* crow = C + static_cast<long long>(m0 + ty * 16 + i) * N + n0 + tx * 4;
+        *reinterpret_cast<ulonglong2*>(crow) = make_ulonglong2(acc[i][0], acc[i][1]);
+    }
+}
+
+template <int BK, int ST, bool B_OUTER>
+static void run16(const char* name, const float* At, const float* B, float* C, const float* Cref, int n,
+                  size_t bytes) {
+    auto k = sgemm_16x4<BK, ST, B_OUTER>;
+    const int smem = ST * BK * 256 * 4;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int tiles = (n / 128) * (n / 128);
+    for (int i = 0; i < 3; ++i) k<<<tiles, 256, smem>>>(At, B, C, n, n, n);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e9;
+    for (int i = 0; i < 20; ++i) {
+        cudaEventRecord(e0);
+        k<<<tiles, 256, smem>>>(At, B, C, n, n, n);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        best = ms < best ? ms : best;
+    }
+    std::vector<float> h(bytes / 4), r(bytes / 4);
+    cudaMemcpy(h.data(), C, bytes, cudaMemcpyDeviceToHost);
+    cudaMemcpy(r.data(), Cref, bytes, cudaMemcpyDeviceToHost);
+    const bool same = memcmp(h.data(), r.data(), bytes) == 0;
+    printf("{\"variant\": \"%s\", \"ms_min\": %.4f, \"tflops\": %.2f, \"bit_identical\": %s, \"err\": \"%s\"}\n", name,
+           best, 2.0 * n * n * (double)n / (best * 1e-3) / 1e12, same ? "true" : "false",
+           cudaGetErrorString(cudaGetLastError()));
+}
+
 template <int BK, int ST, bool DIAG = false>
 static void run(const char* name, const float* At, const float* B, float* C, const float* Cref, int n, size_t bytes) {
     auto k = DIAG ? sgemm_diag<BK, ST> : sgemm_v<BK, ST>;
@@ -272,5 +391,9 @@ int main(int argc, char** argv) {
     run<16, 4, true>("diag k16s4", At, B, C, C0, n, bytes);
     run<32, 2, true>("diag k32s2", At, B, C, C0, n, bytes);
     run<16, 3>("k16s3 (again)", At, B, C, C0, n, bytes);
+    run16<16, 3, true>("16x4 b-outer k16s3", At, B, C, C0, n, bytes);
+    run16<16, 3, false>("16x4 a-outer k16s3", At, B, C, C0, n, bytes);
+    run16<32, 2, true>("16x4 b-outer k32s2", At, B, C, C0, n, bytes);
+    run16<8, 4, true>("16x4 b-outer k8s4", At, B, C, C0, n, bytes);
     return 0;
 }
