@@ -2,12 +2,13 @@
 //
 // The tensor-core half of the diverse kernel pair (§IV-D; attached
 // through the kernel-variant slot of /root/reference/pkg/src/hetrt/api.py:131-138).
-// C = A·B, row-major fp32.  Both UMMA operands are K-major: tcgen05 kind::tf32
-// executes MN-major (transposed) smem operands as a no-op on this part
-// (tools/tc_probe.cu, variants v0/v8-v11), so B is first transposed to
-// B^T (N x K) by a tiled pre-pass (~2·|B| bytes of HBM traffic, a few % of
-// the GEMM), fused with round-to-nearest tf32 conversion (A gets the same RN
-// rounding in a vectorised pass) or with the hi/lo split in 3xTF32 mode.
+// C = A·B, row-major fp32.  Both UMMA operands are K-major.  The operands are
+// RN-rounded to tf32 first (truncation would bias the sum), and B's rounding
+// pass also transposes it to B^T (N x K): ~2·|B| bytes of HBM traffic either
+// way, the same as rounding B in place.  (An MN-major tf32 B would need the
+// 32-byte-atom 128B swizzle, descriptor layout type 1: tools/tc_probe.cu v12.)
+// A gets the same RN rounding in a vectorised pass; 3xTF32 / 3xBF16 modes do
+// the hi/lo splits in the same passes.
 //
 // Structure (persistent, warp-specialised, one CTA per SM):
 //   warp 0      TMA producer: A box {32k x 128m} + B^T box {32k x 256n} per

@@ -1,13 +1,17 @@
 // Stage-by-stage probe of the tcgen05 GEMM building blocks (debug tool).
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O2 -std=c++17 -o tools/tc_probe tools/tc_probe.cu -lcuda
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O2 -std=c++17 -Ipaper_1405_2912_b200/csrc -Iinclude \
+//        -o tools/tc_probe tools/tc_probe.cu -lcuda -Lpaper_1405_2912_b200 -lhetft \
+//        -Xlinker -rpath,'$ORIGIN/../paper_1405_2912_b200'
 // Prints PASS/FAIL lines per stage.
 #include "../paper_1405_2912_b200/csrc/gemm_tc.cu"
 
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 using namespace hf::tc;
+constexpr int B_STAGE = 256 * 32 * 4;  // one 256n x 32k fp32 B tile
 
 // 1. TMEM roundtrip: st 32x32b.x32 then ld
 __global__ void tmem_roundtrip(float* out) {
@@ -68,7 +72,8 @@ __global__ void tma_dump(const __grid_constant__ CUtensorMap tmA, const __grid_c
 // 4. One k-block of MMAs on TMA-filled smem with a sentinel-prefilled
 // accumulator; variant selects descriptor hypotheses.
 __global__ void mma_probe(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                          const __grid_constant__ CUtensorMap tmBt, float* out, int variant) {
+                          const __grid_constant__ CUtensorMap tmBt, const __grid_constant__ CUtensorMap tmB32,
+                          float* out, int variant) {
     extern __shared__ uint8_t raw[];
     uint8_t* smem = raw + ((1024 - (smem_u32(raw) & 1023)) & 1023);
     uint8_t* sa = smem;
@@ -77,7 +82,7 @@ __global__ void mma_probe(const __grid_constant__ CUtensorMap tmA, const __grid_
     uint64_t* bar2 = bar + 1;
     __shared__ uint32_t base;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const bool kmajorB = (variant & 4) != 0;
+    const bool kmajorB = variant < 12 && (variant & 4) != 0;
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
         mbar_init(bar2, 1);
@@ -97,7 +102,9 @@ __global__ void mma_probe(const __grid_constant__ CUtensorMap tmA, const __grid_
             tma_load_2d(sb, &tmBt, bar, 0, 0);
             tma_load_2d(sb + B_STAGE / 2, &tmBt, bar, 0, 128);
         } else {
-            for (int j = 0; j < 8; ++j) tma_load_2d(sb + j * 4096, &tmB, bar, 32 * j, 0);
+            // variants >= 12: B boxes written with the 32-byte-atom 128B swizzle
+            const CUtensorMap* mb = variant >= 12 ? &tmB32 : &tmB;
+            for (int j = 0; j < 8; ++j) tma_load_2d(sb + j * 4096, mb, bar, 32 * j, 0);
         }
     }
     mbar_wait(bar, 0);
@@ -119,7 +126,10 @@ __global__ void mma_probe(const __grid_constant__ CUtensorMap tmA, const __grid_
             idesc &= ~(0x1Fu << 24);
             idesc |= (128u >> 4) << 23;
         }
-        if (kmajorB) idesc &= ~(1u << 16);
+        // make_idesc is K-major for both operands; the MN-major variants set the
+        // B-transpose bit (bit 16).  (An earlier version of this probe only ever
+        // cleared it, so its "MN-major" runs were K-major reads of MN-major data.)
+        if (!kmajorB) idesc |= 1u << 16;
         if (variant & 2) idesc &= ~((2u << 7) | (2u << 10));  // format codes 0
         for (int kk = 0; kk < 4; ++kk) {
             uint64_t ad = make_desc(smem_u32(sa) + kk * 32, 16, 1024);
@@ -133,6 +143,17 @@ __global__ void mma_probe(const __grid_constant__ CUtensorMap tmA, const __grid_
             }
             if (variant == 11) {  // N = 32: single MN atom, LBO irrelevant
                 idesc = (make_idesc(128, 256) & ~(0x3Fu << 17)) | ((32u >> 3) << 17);
+            }
+            if (variant >= 12) {
+                // MN-major tf32: SWIZZLE_128B_BASE32B (layout type 1) is the
+                // only layout CUTLASS's SM100 builder allows for it.
+                // 12: LBO 4096 (next 32-column MN atom), SBO 512 (next 4-row K group)
+                // 13: the two swapped; 14: LBO 4096, SBO 1024 with layout type 2;
+                // 15: LBO 4096, SBO 1024 with layout type 1
+                const uint32_t lbo = variant == 13 ? 512 : 4096;
+                const uint32_t sbo = variant == 13 ? 4096 : (variant == 12 ? 512 : 1024);
+                bd = make_desc(smem_u32(sb) + kk * 1024, lbo, sbo);
+                bd = (bd & ~(7ull << 61)) | ((variant == 14 ? 2ull : 1ull) << 61);
             }
             tc_mma_tf32(base, ad, bd, idesc, 1);
         }
@@ -162,7 +183,7 @@ static CUtensorMap mk(const void* base, uint64_t inner, uint64_t outer, uint32_t
     return m;
 }
 
-int main() {
+int main(int argc, char** argv) {
     cudaSetDevice(0);
     // --- 1
     float* d;
@@ -231,6 +252,11 @@ int main() {
         std::vector<float> Ar(M * K), Br(K * N), Bt(N * K);
         for (int i = 0; i < M * K; ++i) Ar[i] = static_cast<float>((i * 7) % 5);
         for (int i = 0; i < K * N; ++i) Br[i] = static_cast<float>((i * 3) % 7);
+        if (getenv("TC_PROBE_EYE")) {  // C - 5 then shows which (k, n % 32) of B each output read
+            for (int i = 0; i < M * K; ++i) Ar[i] = (i % K) == ((i / K) % K) ? 1.f : 0.f;
+            for (int k = 0; k < K; ++k)
+                for (int n = 0; n < N; ++n) Br[k * N + n] = static_cast<float>(k + 32 * (n % 32));
+        }
         for (int k = 0; k < K; ++k)
             for (int n = 0; n < N; ++n) Bt[n * K + k] = Br[k * N + n];
         float* dBt;
@@ -239,6 +265,17 @@ int main() {
         cudaMemcpy(dB, Br.data(), Br.size() * 4, cudaMemcpyHostToDevice);
         cudaMemcpy(dBt, Bt.data(), Bt.size() * 4, cudaMemcpyHostToDevice);
         CUtensorMap tA = mk(dA, K, M, BK, BM), tB = mk(dB, N, K, 32, BK), tBt = mk(dBt, K, N, BK, 128);
+        CUtensorMap tB32;
+        {
+            cuuint64_t dims[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(K)};
+            cuuint64_t strides[1] = {static_cast<cuuint64_t>(N) * 4};
+            cuuint32_t box[2] = {32, static_cast<cuuint32_t>(BK)};
+            cuuint32_t estr[2] = {1, 1};
+            CUresult r = get_encode()(&tB32, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dB, dims, strides, box, estr,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            printf("tB32 encode: %d\n", static_cast<int>(r));
+        }
         cudaFuncSetAttribute(mma_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
         std::vector<float> ref(M * N);
         for (int i = 0; i < M; ++i)
@@ -247,9 +284,30 @@ int main() {
                 for (int k = 0; k < K; ++k) acc += Ar[i * K + k] * Br[k * N + n];
                 ref[i * N + n] = acc;
             }
-        for (int variant : {0, 4, 8, 9, 10, 11}) {
+        if (argc > 1 && std::string(argv[1]) == "dump32") {
+            // Where TMA's SWIZZLE_128B_ATOM_32B puts B's 32-byte chunks: row k, chunk c -> chunk
+            std::vector<float> iota(K * N);
+            for (int i = 0; i < K * N; ++i) iota[i] = static_cast<float>(i);
+            cudaMemcpy(dB, iota.data(), iota.size() * 4, cudaMemcpyHostToDevice);
+            cudaFuncSetAttribute(tma_dump, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+            tma_dump<<<1, 128, 64 * 1024>>>(ta, tB32, oA, oB);
+            cudaDeviceSynchronize();
+            cudaMemcpy(hB.data(), oB, 4096, cudaMemcpyDeviceToHost);
+            for (int r = 0; r < 12; ++r) {
+                printf("dump32 row %2d:", r);
+                for (int q = 0; q < 4; ++q) {  // smem chunk q holds source chunk ...
+                    const int col = static_cast<int>(hB[r * 32 + q * 8]) - r * N;
+                    printf(" %d", col / 8);
+                }
+                printf("\n");
+            }
+            return 0;
+        }
+        std::vector<int> variants = {12, 13, 14, 15, 4, 0, 9, 10, 11, 8};
+        if (argc > 1) variants = {atoi(argv[1])};  // one variant per process: a fault poisons the context
+        for (int variant : variants) {
             cudaMemset(dC, 0, M * N * 4);
-            mma_probe<<<1, 128, 80 * 1024>>>(tA, tB, tBt, dC, variant);
+            mma_probe<<<1, 128, 80 * 1024>>>(tA, tB, tBt, tB32, dC, variant);
             e = cudaDeviceSynchronize();
             cudaMemcpy(hC.data(), dC, hC.size() * 4, cudaMemcpyDeviceToHost);
             int nb = 0, n5 = 0, nb32 = 0;
@@ -259,6 +317,11 @@ int main() {
                 if (i % N < 32) nb32 += hC[i] != ref[i];
             }
             printf("  (first-32-column mismatches: %d)\n", nb32);
+            if (argc > 2) {  // raw C (fp32, 128 x 256) for offline analysis
+                FILE* f = fopen(argv[2], "wb");
+                fwrite(hC.data(), 4, hC.size(), f);
+                fclose(f);
+            }
             printf("mma_probe v%d: %s (err=%s bad=%d sentinel_only=%d; C[0,0]=%g ref %g; C[1,2]=%g ref %g)\n", variant,
                    nb ? "FAIL" : "PASS", cudaGetErrorString(e), nb, n5, hC[0], ref[0], hC[N + 2], ref[N + 2]);
             if (e != cudaSuccess) break;
