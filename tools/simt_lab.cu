@@ -113,6 +113,111 @@ sgemm_v(const float* __restrict__ At, const float* __restrict__ B, float* __rest
     }
 }
 
+// m-pair form: FFMA2 pairs run along m (the A^T float4s), b is the broadcast
+// scalar.  Same per-output fma chain as sgemm_v, so bit-identical results.
+template <int BK, int ST, bool PAIR_OUTER>
+__global__ void __launch_bounds__(256, 2)
+sgemm_mpair(const float* __restrict__ At, const float* __restrict__ B, float* __restrict__ C, int M, int N, int K) {
+    constexpr int BM = 128, BN = 128;
+    extern __shared__ __align__(16) float sm[];
+    float* As = sm;
+    float* Bs = sm + ST * BK * BM;
+    const int t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31;
+    const int ty = (warp >> 1) * 4 + (lane >> 3);
+    const int tx = (warp & 1) * 8 + (lane & 7);
+    const int tiles_n = N / BN, tiles_m = M / BM;
+    const int group = 8, bid = blockIdx.x, per_group = group * tiles_n;
+    const int g = bid / per_group, first_m = g * group;
+    const int gm = min(tiles_m - first_m, group);
+    const int tm = first_m + (bid % per_group) % gm, tn = (bid % per_group) / gm;
+    const int m0 = tm * BM, n0 = tn * BN;
+    const int c_row = t >> 5, c_col = (t & 31) * 4;
+    const float* Ag = At + static_cast<long long>(c_row) * M + m0 + c_col;
+    const float* Bg = B + static_cast<long long>(c_row) * N + n0 + c_col;
+    auto issue = [&](int kt, int stage) {
+        const long long ka = static_cast<long long>(kt) * BK * M;
+        const long long kb = static_cast<long long>(kt) * BK * N;
+        float* as = As + stage * BK * BM + c_row * BM + c_col;
+        float* bs = Bs + stage * BK * BN + c_row * BN + c_col;
+#pragma unroll
+        for (int r = 0; r < BK; r += 8) {
+            cp_async16(as + r * BM, Ag + ka + static_cast<long long>(r) * M);
+            cp_async16(bs + r * BN, Bg + kb + static_cast<long long>(r) * N);
+        }
+    };
+    // acc[p][j] holds rows (2p, 2p+1) of column j: the pair runs along m
+    unsigned long long acc[4][8];
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[p][j] = 0ull;
+    const int nk = K / BK;
+#pragma unroll
+    for (int s = 0; s < ST - 1; ++s) {
+        if (s < nk) issue(s, s);
+        cp_async_commit();
+    }
+    for (int kt = 0; kt < nk; ++kt) {
+        cp_async_wait<ST - 2>();
+        __syncthreads();
+        {
+            const int nt = kt + ST - 1;
+            if (nt < nk) issue(nt, nt % ST);
+            cp_async_commit();
+        }
+        const float* as = As + (kt % ST) * BK * BM;
+        const float* bs = Bs + (kt % ST) * BK * BN;
+        float4 fa[2][2], fb[2][2];
+        fa[0][0] = *reinterpret_cast<const float4*>(as + ty * 4);
+        fa[0][1] = *reinterpret_cast<const float4*>(as + 64 + ty * 4);
+        fb[0][0] = *reinterpret_cast<const float4*>(bs + tx * 4);
+        fb[0][1] = *reinterpret_cast<const float4*>(bs + 64 + tx * 4);
+#pragma unroll
+        for (int k = 0; k < BK; ++k) {
+            const int cur = k & 1, nxt = cur ^ 1;
+            if (k + 1 < BK) {
+                fa[nxt][0] = *reinterpret_cast<const float4*>(as + (k + 1) * BM + ty * 4);
+                fa[nxt][1] = *reinterpret_cast<const float4*>(as + (k + 1) * BM + 64 + ty * 4);
+                fb[nxt][0] = *reinterpret_cast<const float4*>(bs + (k + 1) * BN + tx * 4);
+                fb[nxt][1] = *reinterpret_cast<const float4*>(bs + (k + 1) * BN + 64 + tx * 4);
+            }
+            const unsigned long long a[4] = {pack2(fa[cur][0].x, fa[cur][0].y), pack2(fa[cur][0].z, fa[cur][0].w),
+                                             pack2(fa[cur][1].x, fa[cur][1].y), pack2(fa[cur][1].z, fa[cur][1].w)};
+            const float b[8] = {fb[cur][0].x, fb[cur][0].y, fb[cur][0].z, fb[cur][0].w,
+                                fb[cur][1].x, fb[cur][1].y, fb[cur][1].z, fb[cur][1].w};
+            if (PAIR_OUTER) {
+#pragma unroll
+                for (int p = 0; p < 4; ++p)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) ffma2(acc[p][j], pack2(b[j], b[j]), a[p]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const unsigned long long bj = pack2(b[j], b[j]);
+#pragma unroll
+                    for (int p = 0; p < 4; ++p) ffma2(acc[p][j], bj, a[p]);
+                }
+            }
+        }
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int row = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+        float* crow = C + static_cast<long long>(row) * N + n0;
+        float r[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            float lo, hi;
+            asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(acc[i / 2][j]));
+            r[j] = (i & 1) ? hi : lo;
+        }
+        *reinterpret_cast<float4*>(crow + tx * 4) = make_float4(r[0], r[1], r[2], r[3]);
+        *reinterpret_cast<float4*>(crow + 64 + tx * 4) = make_float4(r[4], r[5], r[6], r[7]);
+    }
+}
+
 template <int BK, int ST>
 __global__ void __launch_bounds__(256, 2)
 sgemm_diag(const float* __restrict__ At, const float* __restrict__ B, float* __restrict__ C, int M, int N, int K) {
@@ -336,9 +441,10 @@ static void run16(const char* name, const float* At, const float* B, float* C, c
            cudaGetErrorString(cudaGetLastError()));
 }
 
-template <int BK, int ST, bool DIAG = false>
+template <int BK, int ST, bool DIAG = false, int MPAIR = 0>
 static void run(const char* name, const float* At, const float* B, float* C, const float* Cref, int n, size_t bytes) {
-    auto k = DIAG ? sgemm_diag<BK, ST> : sgemm_v<BK, ST>;
+    auto k = MPAIR == 1 ? sgemm_mpair<BK, ST, true> : MPAIR == 2 ? sgemm_mpair<BK, ST, false>
+           : DIAG ? sgemm_diag<BK, ST> : sgemm_v<BK, ST>;
     const int smem = ST * BK * 256 * 4;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int tiles = (n / 128) * (n / 128);
@@ -387,6 +493,9 @@ int main(int argc, char** argv) {
     init<<<1184, 256>>>(At, (size_t)n * n, 1);
     init<<<1184, 256>>>(B, (size_t)n * n, 2);
     run<16, 3>("k16s3 (product)", At, B, C0, nullptr, n, bytes);
+    run<16, 3, false, 1>("m-pair pair-outer k16s3", At, B, C, C0, n, bytes);
+    run<16, 3, false, 2>("m-pair scalar-outer k16s3", At, B, C, C0, n, bytes);
+    run<32, 2, false, 1>("m-pair pair-outer k32s2", At, B, C, C0, n, bytes);
     run<16, 3, true>("diag k16s3", At, B, C, C0, n, bytes);
     run<16, 4, true>("diag k16s4", At, B, C, C0, n, bytes);
     run<32, 2, true>("diag k32s2", At, B, C, C0, n, bytes);
