@@ -1,0 +1,31 @@
+import json, sys
+sys.path.insert(0, ".")
+import torch
+from paper_1405_2912_b200 import kernels
+st = torch.cuda.Stream(); ws = kernels.VoteWorkspace(0, stream=st)
+def time_it(reps, iters=30):
+    torch.cuda.synchronize()
+    with torch.cuda.stream(st):
+        for _ in range(3): kernels.vote_async(reps, ws, 1e-3, stream=st)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(iters): kernels.vote_async(reps, ws, 1e-3, stream=st)
+        e1.record(st)
+    st.synchronize(); return round(e0.elapsed_time(e1) * 1e3 / iters, 2)
+def seg(t):
+    p = t.data_ptr()
+    for s in torch.cuda.memory_snapshot():
+        if s["address"] <= p < s["address"] + s["total_size"]:
+            return {"seg_mib": s["total_size"] >> 20, "off_mib": (p - s["address"]) >> 20}
+m = 4096 * 4096
+base = torch.rand(m, device="cuda") + 1
+noisy = [base * (1 + 1e-6 * torch.randn(m, device="cuda")) for _ in range(2)]
+print("noisy", time_it(noisy), [seg(t) for t in noisy], flush=True)
+fresh = [torch.empty(m, device="cuda") for _ in range(2)]
+for f, x in zip(fresh, noisy): f.copy_(x)
+print("fresh_copies", time_it(fresh), [seg(t) for t in fresh], flush=True)
+print("noisy_again", time_it(noisy), flush=True)
+print("mixed", time_it([noisy[0], fresh[1]]), time_it([fresh[0], noisy[1]]), flush=True)
+print("base_pair", time_it([base, fresh[0]]), seg(base), flush=True)
+for s in torch.cuda.memory_snapshot():
+    print("segment", s["total_size"] >> 20, [(b["size"] >> 20, b["state"]) for b in s["blocks"]])
