@@ -1,6 +1,7 @@
 import json, sys
 sys.path.insert(0, ".")
 import subprocess
+import time
 import torch
 from paper_1405_2912_b200 import kernels
 st = torch.cuda.Stream(); ws = kernels.VoteWorkspace(0, stream=st)
@@ -10,9 +11,13 @@ def time_it(reps, iters=30):
         for _ in range(3): kernels.vote_async(reps, ws, 1e-3, stream=st)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
+        h0 = time.perf_counter()
         for _ in range(iters): kernels.vote_async(reps, ws, 1e-3, stream=st)
+        h1 = time.perf_counter()
         e1.record(st)
-    st.synchronize(); return round(e0.elapsed_time(e1) * 1e3 / iters, 2)
+    st.synchronize()
+    # device us per vote, host enqueue us per vote: device >= host means the GPU waited on the host
+    return round(e0.elapsed_time(e1) * 1e3 / iters, 2), round((h1 - h0) * 1e6 / iters, 2)
 def clocks():
     q = subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm,clocks.mem,power.draw,clocks_throttle_reasons.active",
                         "--format=csv,noheader,nounits", "-i", "0"], capture_output=True, text=True).stdout.strip()
