@@ -1,24 +1,31 @@
 """Benchmark of the voted-task hot path (driver contract: one JSON line).
 
-Workload (BASELINE.json configs[1], "C2"): dual-modular redundancy of a
-4096x4096 fp32 matmul task on one B200 — the tcgen05 TF32 variant (unit
-gpu0.tc) and the SIMT FP32 variant (unit gpu0.simt) run as replicas through
-the drop-in Runtime (DMR strategy), protected attempts checkpoint their
-device-resident inputs (hf_checkpoint into a reserve HBM space), seeded
-bit-flip faults are injected at a fixed per-replica probability, hf_vote
-decides, mismatches are re-run.  A "step" is one voted task.
+Headline workload (BASELINE.json north_star / metric): HetTMR of a 4096x4096
+fp32 matmul task on one B200 — three diverse replicas, the tcgen05 TF32
+variant (unit gpu0.tc), the SIMT FP32 variant (gpu0.simt) and the tcgen05
+3xBF16 variant (gpu0.tc3) — through the drop-in Runtime: protected attempts
+checkpoint their device-resident inputs (hf_checkpoint into a reserve HBM
+space), every replica draws seeded bit-flip faults at a fixed probability,
+hf_vote (K = 3) commits the majority (a single faulty replica is corrected
+in place), an element without a majority re-runs.  A "step" is one voted
+task.
 
   value  tasks/s with A, B already resident in HBM (sole device copies)
   e2e    tasks/s through the same public API with HOST buffers: per step the
-         pinned inputs are copied host->device inside invoke() and the
-         committed C is read back device->host (read_into)
+         pinned inputs are copied host->device inside the task and the
+         committed C is read back device->host (read_into_async)
+  dmr    BASELINE configs[1] (HetDMR, TC vs SIMT, detect-and-rerun), extra key
 N > 1: one process per GPU, each running its own independent task stream
-(weak scaling, no data-path collective); timing is max over ranks.
+(weak scaling, no data-path collective); timing is max over ranks.  With
+N >= 3, rank 0 also runs configs[2] ("c3": the three replicas on GPUs 0/1/2,
+the vote sliced over them reading peer replicas over NVLink).
 
 --impl reference times the reference's own CPU implementation of the same
-task (hetrt from baseline/_ref through its public Runtime API, numpy bodies,
-its voting.compare) on the host cores; without baseline/_ref the oracle port
-(oracle/: numpy matmul + restated voter) is timed instead.
+task on the host cores: hetrt from baseline/_ref (its MemoryManager with a
+protected checkpoint of the inputs, simulate_execution with the reference
+fault model around three numpy fp32 matmul bodies, voting.compare on the
+pairs (0,1), (0,2), (1,2), commit of an agreeing replica).  Without
+baseline/_ref the oracle port (oracle/: numpy + restated voter) is timed.
 """
 
 from __future__ import annotations
@@ -52,7 +59,10 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None, help="default max(80, --steps)")
     ap.add_argument("--depth", type=int, default=1, help="TaskStream depth (tasks in flight beyond the one settling)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-tmr", action="store_true", help="skip the HetTMR 4096^2 side measurement")
+    ap.add_argument("--no-dmr", action="store_true", help="skip the HetDMR (configs[1]) side measurement")
+    ap.add_argument("--no-c3", action="store_true", help="skip the replicas-on-3-GPUs sub-measurement (N >= 3)")
+    ap.add_argument("--c3-devices", default=None,
+                    help="run the c3 sub-measurement on these GPUs at any N (e.g. 0,0,0: one-GPU code-path check)")
     ap.add_argument("--detect-probes", type=int, default=2000)
     ap.add_argument("--cpu-sample-s", type=float, default=12.0)
     ap.add_argument("--trace-steps", action="store_true", help="per-step host wall times to stderr")
@@ -136,47 +146,113 @@ def _reference_module():
     return None
 
 
-def reference_tasks(n: int, count_or_seconds, seed: int, by_time: bool):
-    """Run DMR n x n matmul tasks with the reference CPU implementation.
-    Returns (tasks, seconds, kind, detail)."""
-    hetrt = _reference_module()
+METRIC = "voted tasks/sec (HetTMR 4096^2 fp32 matmul, 3 diverse replicas, majority vote)"
+
+
+def bench_config(args, world: int) -> dict:
+    """The workload both arms report (identical dict: the driver compares them)."""
+    n = args.n
+    return {"workload": f"HetTMR {n}x{n} fp32 matmul: 3 diverse replicas (tcgen05 TF32, SIMT FP32, "
+                        f"tcgen05 3xBF16; reference arm: 3 numpy fp32 bodies), protected checkpoint of the "
+                        f"inputs, per-replica fault p={args.fault_prob}, K=3 majority vote, re-run without "
+                        f"majority",
+            "n": n, "replicas": 3, "strategy": "hettmr", "fault_prob": args.fault_prob,
+            "parallelism": f"independent task streams x{world}",
+            "l2": "operands (4 x 64 MiB per task) exceed the 126 MB L2; no flush needed"}
+
+
+def _ref_tmr_runner(hetrt, n, seed, fault_prob):
+    """One HetTMR n x n task through the reference's own pieces (it has no
+    TMR strategy; its Runtime only runs DMR, executor.py:225-285): the
+    reference MemoryManager with the inputs as sole copies in a device space
+    (so protected requests checkpoint them, memory.py:176-189), three units of
+    its fault model (corrupt_prob = fault_prob, its CorruptionSpec) running
+    numpy fp32 matmul bodies through simulate_execution (devices.py:223-259),
+    voting.compare on every pair (voting.py:106-123) with the result bytes
+    copied out as Executor._vote does (executor.py:319-325), commit of a
+    replica that agrees with another, otherwise a re-run of all three.
+    Returns (run_one, setup_one): setup registers a task's areas (untimed)."""
+    from hetrt import memory as rmem
+    from hetrt import voting as rvote
+    from hetrt.devices import FaultClass, ValueType, simulate_execution
+    f32 = ValueType.FLOAT32
+    cfg = {"memory_spaces": [{"id": "host", "host": True}, {"id": "dev"}],
+           "units": [{"id": f"cpu{i}", "kind": "cpu", "memory_space": "dev", "corrupt_prob": fault_prob,
+                      "seed": seed * 1_000_003 + i * 101 + 31} for i in range(3)]}
+    fleet = hetrt.load_fleet(cfg)
+    units = [fleet.units[f"cpu{i}"] for i in range(3)]
+    vcfg = rvote.VoterConfig()
     rng = np.random.default_rng(seed)
-    a = rng.uniform(1, 2, (n, n)).astype(np.float32)
-    b = rng.uniform(1, 2, (n, n)).astype(np.float32)
+    a = rng.uniform(1, 2, (n, n)).astype(np.float32).tobytes()
+    b = rng.uniform(1, 2, (n, n)).astype(np.float32).tobytes()
+    zeros = bytes(4 * n * n)
+
+    def setup():
+        # a fresh manager per task: the reference has no area release, and the
+        # areas of finished tasks would otherwise pile up (6 x 64 MiB each)
+        mm = rmem.MemoryManager(fleet)
+        ia = mm.register(a, n * n, f32, "r")
+        ib = mm.register(b, n * n, f32, "r")
+        ic = mm.register(zeros, n * n, f32, "w")
+        for x in (ia, ib):            # device-resident sole copies (the GPU arm's register_device_data)
+            h = mm.request(x, "dev", "rw")
+            mm.commit_success([h])
+        return mm, ia, ib, ic
+
+    def run(areas):
+        mm, ia, ib, ic = areas
+        rounds = 0
+        while True:
+            rounds += 1
+            hcs = []
+            for u in units:
+                while True:
+                    ha = mm.request(ia, "dev", "r", protect=True)
+                    hb = mm.request(ib, "dev", "r", protect=True)
+                    hc = mm.request(ic, "dev", "w", protect=True)
+                    A = np.frombuffer(ha.payload, np.float32).reshape(n, n)
+                    B = np.frombuffer(hb.payload, np.float32).reshape(n, n)
+                    C = np.frombuffer(hc.payload, np.float32).reshape(n, n)
+                    out = simulate_execution(u, "mm_cpu", "cpu", n * n, body=lambda: np.matmul(A, B, out=C),
+                                             write_views=[(C.reshape(-1), f32)])
+                    if out.fault in (None, FaultClass.CORRUPT):
+                        hcs.append(hc)
+                        break
+            res = [{ic: (bytes(h.payload), f32, 4)} for h in hcs]
+            agree = [False] * 3
+            for i, j in ((0, 1), (0, 2), (1, 2)):
+                if rvote.compare(res[i], res[j], vcfg).verdict == "match":
+                    agree[i] = agree[j] = True
+            if any(agree):
+                mm.commit_success([hcs[agree.index(True)]])
+                return rounds
+    return run, setup
+
+
+def reference_tasks(n: int, count_or_seconds, seed: int, by_time: bool, fault_prob: float = 0.05,
+                    max_seconds: float = 1e9):
+    """Run HetTMR n x n matmul tasks with the reference CPU implementation.
+    Returns (tasks, seconds, kind, detail); only the tasks are timed (the
+    per-task area registration is not)."""
+    hetrt = _reference_module()
     if hetrt is not None:
-        cfg = {"memory_spaces": [{"id": "host", "host": True}],
-               "units": [{"id": "cpu0", "kind": "cpu", "memory_space": "host", "seed": 1},
-                         {"id": "cpu1", "kind": "cpu", "memory_space": "host", "seed": 2}]}
-        rt = hetrt.Runtime(hetrt.load_fleet(cfg), hetrt.RuntimeConfig(serial_replicas=True))
-        task = rt.declare_task("matmul", (hetrt.Param.area("A", "r"), hetrt.Param.area("B", "r"),
-                                          hetrt.Param.area("C", "w"), hetrt.Param.scalar("n")))
-
-        def body(ctx):
-            k = ctx.arg("n")
-            A = ctx.request("A", "r").reshape(k, k)
-            B = ctx.request("B", "r").reshape(k, k)
-            C = ctx.request("C", "w").reshape(k, k)
-            np.matmul(A, B, out=C)
-
-        rt.attach_kernel(task, "mm_cpu", "cpu", body)
-        zeros = bytes(4 * n * n)
-
-        def one():
-            ia = rt.register_data(a.tobytes(), n * n, hetrt.ValueType.FLOAT32, "r")
-            ib = rt.register_data(b.tobytes(), n * n, hetrt.ValueType.FLOAT32, "r")
-            ic = rt.register_data(zeros, n * n, hetrt.ValueType.FLOAT32, "w")
-            rep = rt.invoke(task, {"A": ia, "B": ib, "C": ic, "n": n}, hetrt.Strategy(hetrt.StrategyKind.DMR))
-            rt.read_area(ic)
-            assert rep.success
-        kind, detail = "reference", "hetrt (baseline/_ref) Runtime.invoke DMR: 2 numpy matmul bodies + voting.compare"
+        run, setup = _ref_tmr_runner(hetrt, n, seed, fault_prob)
+        kind = "reference"
+        detail = ("hetrt (baseline/_ref): MemoryManager protected checkpoint, 3 numpy fp32 matmul bodies "
+                  "via simulate_execution (reference fault model), voting.compare on pairs (0,1),(0,2),(1,2)")
     else:
         from oracle import vote as ovote
+        rng = np.random.default_rng(seed)
+        a = rng.uniform(1, 2, (n, n)).astype(np.float32)
+        b = rng.uniform(1, 2, (n, n)).astype(np.float32)
 
-        def one():
-            c0 = a @ b
-            c1 = a @ b
-            ovote.vote([c0, c1], 1e-3)
-        kind, detail = "port", "oracle port: 2 numpy matmuls + oracle.vote (reference absent)"
+        def setup():
+            return None
+
+        def run(_):
+            ovote.vote([a @ b, a @ b, a @ b], 1e-3)
+            return 1
+        kind, detail = "port", "oracle port: 3 numpy matmuls + oracle.vote (reference absent)"
     # all host cores for the BLAS matmul bodies: torchrun exports
     # OMP_NUM_THREADS=1 to every rank, which would leave the reference arm
     # single-threaded under the driver's multi-GPU launch
@@ -186,17 +262,18 @@ def reference_tasks(n: int, count_or_seconds, seed: int, by_time: bool):
     except Exception:  # noqa: BLE001 - threadpoolctl absent: numpy's own default
         limiter = None
     try:
-        t0 = time.perf_counter()
-        done = 0
+        spent, done, rounds = 0.0, 0, 0
         while True:
-            one()
+            areas = setup()
+            t0 = time.perf_counter()
+            rounds += run(areas)
+            spent += time.perf_counter() - t0
             done += 1
-            el = time.perf_counter() - t0
-            if by_time and el >= count_or_seconds and done >= 1:
+            if by_time and spent >= count_or_seconds:
                 break
-            if not by_time and done >= count_or_seconds:
+            if not by_time and (done >= count_or_seconds or spent >= max_seconds):
                 break
-        return done, time.perf_counter() - t0, kind, detail
+        return done, spent, kind, f"{detail}; {rounds} rounds"
     finally:
         if limiter is not None:
             limiter.restore_original_limits()
@@ -213,14 +290,16 @@ def run_reference_arm(args, rank, world):
     if rank != 0:
         return
     n = args.n
-    reference_tasks(n, max(1, args.warmup // 3), args.seed, by_time=False)   # warm caches/BLAS
-    tasks, secs, kind, detail = reference_tasks(n, args.steps, args.seed, by_time=False)
+    reference_tasks(n, 1, args.seed, by_time=False, fault_prob=args.fault_prob)   # warm caches/BLAS
+    # bounded: at most ~2 min of CPU work whatever --steps asks
+    tasks, secs, kind, detail = reference_tasks(n, args.steps, args.seed, by_time=False,
+                                                fault_prob=args.fault_prob, max_seconds=120.0)
     v = tasks / secs
-    line = {"metric": "voted tasks/sec (DMR 4096^2 fp32 matmul, TC vs SIMT variants)", "value": v,
+    line = {"metric": METRIC, "value": v,
             "unit": "tasks/s", "n_gpus": args.gpus, "steps": tasks, "warmup": args.warmup,
             "ms_per_step": 1e3 * secs / tasks, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic U[1,2) fp32 operands",
-            "config": {"workload": f"C2: DMR {n}x{n} fp32 matmul, detect-and-rerun", "n": n},
+            "config": bench_config(args, world),
             "impl": "reference",
             "cpu_baseline": {"value": v, "unit": "tasks/s", "cores": host_cores(), "kind": kind,
                              "sample": f"{tasks} tasks: {detail}"},
@@ -230,17 +309,178 @@ def run_reference_arm(args, rank, world):
 
 # ---- B200 arm ---------------------------------------------------------------------------------
 
-def build_runtime(device: int, fault_prob: float, seed: int):
+TMR_KINDS = ("gpu-tc", "gpu-simt", "gpu-tc3")
+DMR_KINDS = ("gpu-tc", "gpu-simt")
+
+
+def build_runtime(device: int, fault_prob: float, seed: int, kinds=TMR_KINDS):
     import paper_1405_2912_b200 as hf
-    cfg = hf.gpu_fleet_config(devices=(device,), kinds=("gpu-tc", "gpu-simt"))
+    cfg = hf.gpu_fleet_config(devices=(device,), kinds=kinds)
     cfg["memory_spaces"].append({"id": f"gpu{device}ckpt", "device": device, "label": "HBM checkpoint reserve"})
     for i, u in enumerate(cfg["units"]):
         u.update({"corrupt_prob": fault_prob, "corrupt_mode": "bitflip", "seed": seed * 1_000_003 + i * 101 + 17})
     fleet = hf.load_fleet(cfg)
     rt = hf.Runtime(fleet, hf.RuntimeConfig(checkpoint_space=f"gpu{device}ckpt", serial_replicas=True,
                                             attempt_limit=64))
-    task = hf.get_workload("matmul").attach(rt, kinds=("gpu-tc", "gpu-simt"))
+    task = hf.get_workload("matmul").attach(rt, kinds=kinds)
     return hf, rt, task
+
+
+class TaskStreamBench:
+    """Voted n x n matmul tasks of one strategy through the drop-in Runtime's
+    TaskStream on one GPU: device-resident inputs (`device_stream`) or host
+    buffers with H2D/D2H inside the stream (`host_stream`)."""
+
+    LOOKAHEAD = 2
+
+    def __init__(self, args, device, rank, kinds, strategy, seed_salt=0, built=None, space=None):
+        import torch
+        self.torch = torch
+        self.args, self.device, self.n = args, device, args.n
+        self.hf, self.rt, self.task = built or build_runtime(device, args.fault_prob,
+                                                             args.seed + 7919 * rank + seed_salt, kinds)
+        hf, n = self.hf, self.n
+        self.nb = n * n * 4
+        self.space = space or f"gpu{device}mem"
+        # pre-size the device heap for the stream's high-water mark (re-dispatched
+        # rounds included): no cudaMalloc inside the timed regions
+        for sp in self.rt.fleet.spaces.values():
+            if sp.device is not None and sp.id != "ckpt" and not sp.id.endswith("ckpt"):
+                self.rt.reserve(sp.id, self.nb, 32 if sp.id == self.space else 12)
+        gen = torch.Generator(device=f"cuda:{device}")
+        gen.manual_seed(args.seed * 7919 + rank)
+        self.A = (torch.rand(n * n, device=f"cuda:{device}", generator=gen) + 1).view(torch.uint8)
+        self.B = (torch.rand(n * n, device=f"cuda:{device}", generator=gen) + 1).view(torch.uint8)
+        self.C0 = torch.zeros(self.nb, dtype=torch.uint8, device=f"cuda:{device}")
+        self.strat = strategy if isinstance(strategy, hf.Strategy) else hf.Strategy(strategy)
+        self.stream = self.rt.backend.stream(device)
+        self.stats = {"tasks": 0, "rounds": 0, "votes": {}, "injected": 0, "mismatch": 0, "corrected": 0,
+                      "vote_ns": 0, "attempt_ns": {}, "attempt_n": {}}
+        self._host = None
+
+    def record(self, rep):
+        st = self.stats
+        st["tasks"] += 1
+        st["rounds"] += rep.rounds
+        for v in rep.votes:
+            st["votes"][v] = st["votes"].get(v, 0) + 1
+        st["injected"] += len(rep.injected)
+        st["mismatch"] += rep.fault_counts["vote_mismatch"]
+        st["corrected"] += rep.fault_counts["vote_corrected"]
+        st["vote_ns"] += rep.voter_ns
+
+    def on_trace(self, line: str):
+        if line.startswith("ATT") and "fault=none" in line:
+            f = dict(kv.split("=", 1) for kv in line.split()[1:] if "=" in kv)
+            k = f["kernel"]
+            self.stats["attempt_ns"][k] = self.stats["attempt_ns"].get(k, 0) + int(f["duration_ns"])
+            self.stats["attempt_n"][k] = self.stats["attempt_n"].get(k, 0) + 1
+
+    def device_stream(self, steps: int, recording: bool):
+        """`steps` voted tasks on device-resident inputs through a TaskStream:
+        task i+1's replicas are queued on the GPU before task i's verdict is
+        read, so host-side settling overlaps kernels."""
+        rt, hf, n = self.rt, self.hf, self.n
+        queue = []
+        with rt.task_stream(depth=self.args.depth) as ts:
+            for _ in range(steps):
+                ia = rt.register_device_data(self.A, n * n, hf.ValueType.FLOAT32, "r", self.space)
+                ib = rt.register_device_data(self.B, n * n, hf.ValueType.FLOAT32, "r", self.space)
+                ic = rt.register_device_data(self.C0, n * n, hf.ValueType.FLOAT32, "w", self.space)
+                queue.append((ts.submit(self.task, {"A": ia, "B": ib, "C": ic, "n": n}, self.strat), (ia, ib, ic)))
+                while queue and queue[0][0].success:
+                    rep, areas = queue.pop(0)
+                    if recording:
+                        self.record(rep)
+                    for x in areas:
+                        rt.release(x)
+        for rep, areas in queue:
+            if not rep.success:
+                raise RuntimeError("task failed")
+            if recording:
+                self.record(rep)
+            for x in areas:
+                rt.release(x)
+
+    def _host_buffers(self):
+        if self._host is None:
+            torch, nb = self.torch, self.nb
+            hA = torch.empty(nb, dtype=torch.uint8).pin_memory()
+            hB = torch.empty(nb, dtype=torch.uint8).pin_memory()
+            hC = torch.empty(nb, dtype=torch.uint8).pin_memory()
+            hZ = torch.zeros(nb, dtype=torch.uint8).pin_memory()
+            hA.copy_(self.A.cpu())
+            hB.copy_(self.B.cpu())
+            self._host = (hA, hB, hC, hZ)
+        return self._host
+
+    def host_stream(self, steps):
+        """Software pipeline over the public API: step i+LOOKAHEAD's inputs go
+        H2D on the copy engine and step i-1's result goes D2H while step i
+        computes; a TaskStream keeps the next task's kernels queued behind the
+        current.  Returns the rounds the tasks took."""
+        rt, hf, n = self.rt, self.hf, self.n
+        hA, hB, hC, hZ = self._host_buffers()
+
+        def stage():
+            ia = rt.register_host_buffer(hA, n * n, hf.ValueType.FLOAT32, "r")
+            ib = rt.register_host_buffer(hB, n * n, hf.ValueType.FLOAT32, "r")
+            ic = rt.register_host_buffer(hZ, n * n, hf.ValueType.FLOAT32, "w")
+            rt.prefetch(ia, self.space)
+            rt.prefetch(ib, self.space)
+            return ia, ib, ic
+
+        # inputs are staged LOOKAHEAD steps ahead, so the copy engine stays
+        # busy while the host blocks on a re-dispatched (mismatching) task
+        staged = [stage() for _ in range(min(self.LOOKAHEAD, steps))]
+        queue, retired, last, reps = [], [], None, []
+        with rt.task_stream(depth=self.args.depth) as ts:
+            for i in range(steps):
+                ia, ib, ic = staged.pop(0)
+                if i + self.LOOKAHEAD < steps:
+                    staged.append(stage())
+                queue.append((ts.submit(self.task, {"A": ia, "B": ib, "C": ic, "n": n}, self.strat), (ia, ib, ic)))
+                reps.append(queue[-1][0])
+                if self.args.trace_steps:
+                    print(f"e2e step {i} t={time.perf_counter():.6f} rounds={queue[-1][0].rounds}", file=sys.stderr)
+                while queue and queue[0][0].success:
+                    rep, areas = queue.pop(0)
+                    last = rt.read_into_async(areas[2], hC)
+                    for x in retired:     # released one step late: their D2H overlapped
+                        rt.release(x)
+                    retired = list(areas)
+        for rep, areas in queue:
+            last = rt.read_into_async(areas[2], hC)
+            retired += list(areas)
+        if last is not None:
+            last.synchronize()
+        for x in retired:
+            rt.release(x)
+        return sum(r.rounds for r in reps)
+
+    def warm(self):
+        self.device_stream(1, False)
+        t0 = time.perf_counter()
+        done = 1
+        while done < self.args.warmup or time.perf_counter() - t0 < 0.8:
+            self.device_stream(max(1, self.args.warmup), False)
+            done += max(1, self.args.warmup)
+        self.torch.cuda.synchronize()
+
+    def timed(self, fn, *a):
+        """CUDA-event time of fn(*a) on the runtime's compute stream (seconds)."""
+        torch = self.torch
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(self.stream)
+        out = fn(*a)
+        e1.record(self.stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1e-3, out
+
+    def kernel_ms(self, kernel: str):
+        c = self.stats["attempt_n"].get(kernel, 0)
+        return self.stats["attempt_ns"].get(kernel, 0) / c * 1e-6 if c else None
 
 
 def run_hetft_arm(args, rank, world, local):
@@ -269,192 +509,91 @@ def run_hetft_arm(args, rank, world, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    hf, rt, task = build_runtime(device, args.fault_prob, args.seed + 7919 * rank)
     from paper_1405_2912_b200 import kernels
     n = args.n
     nb = n * n * 4
-    space = f"gpu{device}mem"
-    # pre-size the device heap for the stream's high-water mark (re-dispatched
-    # rounds included): no cudaMalloc inside the timed regions
-    rt.reserve(space, nb, 24)
-    gen = torch.Generator(device=f"cuda:{device}")
-    gen.manual_seed(args.seed * 7919 + rank)
-    A = (torch.rand(n * n, device=f"cuda:{device}", generator=gen) + 1).view(torch.uint8)
-    B = (torch.rand(n * n, device=f"cuda:{device}", generator=gen) + 1).view(torch.uint8)
-    C0 = torch.zeros(nb, dtype=torch.uint8, device=f"cuda:{device}")
-    strat = hf.Strategy(hf.StrategyKind.HET_DMR)
-    stream = rt.backend.stream(device)
-
-    stats = {"tasks": 0, "rounds": 0, "votes": {}, "injected": 0, "mismatch": 0, "vote_ns": 0,
-             "attempt_ns": {}, "attempt_n": {}}
-
-    def record(rep):
-        stats["tasks"] += 1
-        stats["rounds"] += rep.rounds
-        for v in rep.votes:
-            stats["votes"][v] = stats["votes"].get(v, 0) + 1
-        stats["injected"] += len(rep.injected)
-        stats["mismatch"] += rep.fault_counts["vote_mismatch"]
-        stats["vote_ns"] += rep.voter_ns
-
-    def device_stream(steps: int, recording: bool):
-        """`steps` voted tasks on device-resident inputs through a TaskStream:
-        task i+1's replicas are queued on the GPU before task i's verdict is
-        read, so host-side settling overlaps kernels."""
-        queue = []
-        with rt.task_stream(depth=args.depth) as ts:
-            for _ in range(steps):
-                ia = rt.register_device_data(A, n * n, hf.ValueType.FLOAT32, "r", space)
-                ib = rt.register_device_data(B, n * n, hf.ValueType.FLOAT32, "r", space)
-                ic = rt.register_device_data(C0, n * n, hf.ValueType.FLOAT32, "w", space)
-                queue.append((ts.submit(task, {"A": ia, "B": ib, "C": ic, "n": n}, strat), (ia, ib, ic)))
-                while queue and queue[0][0].success:
-                    rep, areas = queue.pop(0)
-                    if recording:
-                        record(rep)
-                    for x in areas:
-                        rt.release(x)
-        for rep, areas in queue:
-            if not rep.success:
-                raise RuntimeError("task failed")
-            if recording:
-                record(rep)
-            for x in areas:
-                rt.release(x)
-
-    # trace per-kernel durations via the executor's measured attempts
-    def on_trace(line: str):
-        if line.startswith("ATT") and "fault=none" in line:
-            f = dict(kv.split("=", 1) for kv in line.split()[1:] if "=" in kv)
-            k = f["kernel"]
-            stats["attempt_ns"][k] = stats["attempt_ns"].get(k, 0) + int(f["duration_ns"])
-            stats["attempt_n"][k] = stats["attempt_n"].get(k, 0) + 1
+    import paper_1405_2912_b200 as hf
+    tmr = TaskStreamBench(args, device, rank, TMR_KINDS, hf.StrategyKind.HET_TMR)
 
     # the clock sampler starts during warm-up (nvidia-smi needs ~0.5 s to
     # emit its first sample) and stops right after the timed region
     sampler = ClockSampler(device) if rank == 0 else None
-    device_stream(1, False)
     if sampler:
         sampler.start()
-    t_start = time.perf_counter()
-    done = 1
-    while done < args.warmup or time.perf_counter() - t_start < 0.8:
-        device_stream(max(1, args.warmup), False)
-        done += max(1, args.warmup)
-    torch.cuda.synchronize()
+    tmr.warm()
 
     # ---- timed region: device-resident inputs ----
-    rt.executor._trace = on_trace
+    tmr.rt.executor._trace = tmr.on_trace
     barrier()
     torch.cuda.synchronize()
     launches0 = kernels.LAUNCHES
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    device_stream(args.steps, True)
-    ev1.record(stream)
-    torch.cuda.synchronize()
+    t_dev, _ = tmr.timed(tmr.device_stream, args.steps, True)
     barrier()
     clocks = sampler.stop() if sampler else None
     launches = kernels.LAUNCHES - launches0
-    rt.executor._trace = None
-    t_dev = ev0.elapsed_time(ev1) * 1e-3
+    tmr.rt.executor._trace = None
     t_max = max_over_ranks(t_dev)
 
-    # ---- e2e: host buffers through the same API (H2D inside invoke, D2H read) ----
+    # ---- e2e: host buffers through the same API (H2D inside the stream, D2H read) ----
     # at least 80 steps: the pipeline fill (first 128 MiB H2D before any
     # kernel can start) and drain (last D2H) are paid once per timed region
     e2e_steps = args.e2e_steps or max(80, args.steps)
-    hA = torch.empty(nb, dtype=torch.uint8).pin_memory()
-    hB = torch.empty(nb, dtype=torch.uint8).pin_memory()
-    hC = torch.empty(nb, dtype=torch.uint8).pin_memory()
-    hZ = torch.zeros(nb, dtype=torch.uint8).pin_memory()
-    hA.copy_(A.cpu())
-    hB.copy_(B.cpu())
-
-    def stage(i):
-        """Register step i's host inputs and start their H2D on the copy stream."""
-        ia = rt.register_host_buffer(hA, n * n, hf.ValueType.FLOAT32, "r")
-        ib = rt.register_host_buffer(hB, n * n, hf.ValueType.FLOAT32, "r")
-        ic = rt.register_host_buffer(hZ, n * n, hf.ValueType.FLOAT32, "w")
-        rt.prefetch(ia, space)
-        rt.prefetch(ib, space)
-        return ia, ib, ic
-
-    LOOKAHEAD = 2
-
-    def host_stream(steps):
-        """Software pipeline over the public API: step i+1's inputs go H2D on
-        the copy engine and step i-1's result goes D2H while step i computes;
-        a TaskStream keeps the next task's kernels queued behind the current."""
-        # inputs are staged LOOKAHEAD steps ahead, so the copy engine stays
-        # busy while the host blocks on a re-dispatched (mismatching) task
-        staged = [stage(i) for i in range(min(LOOKAHEAD, steps))]
-        queue, retired, last = [], [], None
-        reps = []
-        with rt.task_stream(depth=args.depth) as ts:
-            for i in range(steps):
-                ia, ib, ic = staged.pop(0)
-                if i + LOOKAHEAD < steps:
-                    staged.append(stage(i + LOOKAHEAD))
-                queue.append((ts.submit(task, {"A": ia, "B": ib, "C": ic, "n": n}, strat), (ia, ib, ic)))
-                reps.append(queue[-1][0])
-                if args.trace_steps:
-                    print(f"e2e step {i} t={time.perf_counter():.6f} rounds={queue[-1][0].rounds}", file=sys.stderr)
-                while queue and queue[0][0].success:
-                    rep, areas = queue.pop(0)
-                    last = rt.read_into_async(areas[2], hC)
-                    for x in retired:     # released one step late: their D2H overlapped
-                        rt.release(x)
-                    retired = list(areas)
-        for rep, areas in queue:
-            last = rt.read_into_async(areas[2], hC)
-            retired += list(areas)
-        if last is not None:
-            last.synchronize()
-        for x in retired:
-            rt.release(x)
-        return sum(r.rounds for r in reps)
-
-    host_stream(2)
+    tmr.host_stream(2)
     torch.cuda.synchronize()
     barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    e2e_rounds = host_stream(e2e_steps)
-    e1.record(stream)
-    torch.cuda.synchronize()
+    t_e2e, e2e_rounds = tmr.timed(tmr.host_stream, e2e_steps)
     barrier()
-    t_e2e = max_over_ranks(e0.elapsed_time(e1) * 1e-3)
-    # the result of the last step really arrived: spot-check it against the device copy
-    hC_check = hC.view(torch.float32)[:4].clone()
+    t_e2e = max_over_ranks(t_e2e)
+
+    # ---- BASELINE configs[1]: HetDMR, TC vs SIMT, detect-and-rerun (extra key) ----
+    dmr = None
+    if not args.no_dmr:
+        dmr_b = TaskStreamBench(args, device, rank, DMR_KINDS, tmr.hf.StrategyKind.HET_DMR, seed_salt=13)
+        dmr_b.warm()
+        dmr_steps = max(30, args.steps)
+        t_d, _ = dmr_b.timed(dmr_b.device_stream, dmr_steps, True)
+        dmr_b.host_stream(2)
+        t_de, de_rounds = dmr_b.timed(dmr_b.host_stream, e2e_steps)
+        dmr = {"value": dmr_steps / t_d, "unit": "tasks/s", "steps": dmr_steps, "ms_per_task": 1e3 * t_d / dmr_steps,
+               "workload": f"C2 (BASELINE configs[1]): HetDMR {n}x{n} fp32 matmul, tcgen05-TF32 vs SIMT-FP32, "
+                           f"bit flips p={args.fault_prob}/replica, detect-and-rerun",
+               "e2e": {"value": e2e_steps / t_de, "unit": "tasks/s", "steps": e2e_steps, "rounds": de_rounds,
+                       "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": nb},
+               "votes": dmr_b.stats["votes"], "rounds": dmr_b.stats["rounds"],
+               "voter_gbs_in_task": (2 * nb * sum(dmr_b.stats["votes"].values())) / (dmr_b.stats["vote_ns"] * 1e-9) / 1e9
+               if dmr_b.stats["vote_ns"] else None}
+        del dmr_b
 
     # ---- kernel-level measurements (same process, after the timed regions) ----
     kern = kernel_rooflines(device, n, kernels, torch)
-    # at least 30 timed tasks: a 20-task window swings with the fault draws
-    tmr = tmr_rate(device, n, args.fault_prob, args.seed + 7919 * rank, max(30, args.steps),
-                   max(5, args.warmup), torch) if not args.no_tmr else None
     detect = detect_rate(device, n, kernels, torch, args.seed, probes=args.detect_probes) if rank == 0 else None
+    c3 = None
+    if rank == 0 and not args.no_c3:
+        if world >= 3 and not shared_gpu and torch.cuda.device_count() >= 3:
+            c3 = c3_rate(args, torch, devices=(0, 1, 2))
+        elif args.c3_devices:       # code-path check, e.g. 0,0,0 on a one-GPU box
+            c3 = c3_rate(args, torch, devices=tuple(int(x) for x in args.c3_devices.split(",")))
 
     total_tasks = args.steps * world
     if rank != 0:
         return
     peaks, peak_src = load_peaks()
-    simt_ns = stats["attempt_ns"].get("mm_simt", 0) / max(1, stats["attempt_n"].get("mm_simt", 1))
-    tc_ns = stats["attempt_ns"].get("mm_tc", 0) / max(1, stats["attempt_n"].get("mm_tc", 1))
+    stats = tmr.stats
+    simt_ms, tc_ms, tc3_ms = tmr.kernel_ms("mm_simt"), tmr.kernel_ms("mm_tc"), tmr.kernel_ms("mm_tc3x")
     flops = 2.0 * n ** 3
-    simt_tflops = flops / (simt_ns * 1e-9) / 1e12 if simt_ns else None
+    simt_tflops = flops / (simt_ms * 1e-3) / 1e12 if simt_ms else None
     sm_max = (clocks or {}).get("sm_max_mhz") or 1965.0
     ffma_peak, ffma_src = fp32_peak(sm_max)
     traffic = ncu_traffic("sgemm_128x128", "transpose_a")
-    vote_gbs = (stats["votes"] and stats["vote_ns"]) and \
-        (2 * nb * sum(stats["votes"].values())) / (stats["vote_ns"] * 1e-9) / 1e9
+    vote_gbs = (3 * nb * sum(stats["votes"].values())) / (stats["vote_ns"] * 1e-9) / 1e9 if stats["vote_ns"] else None
     cpu = None
     if not args.no_cpu_baseline:
-        tasks, secs, kind, detail = reference_tasks(n, args.cpu_sample_s, args.seed, by_time=True)
+        tasks, secs, kind, detail = reference_tasks(n, args.cpu_sample_s, args.seed, by_time=True,
+                                                    fault_prob=args.fault_prob)
         cpu = {"value": tasks / secs, "unit": "tasks/s", "cores": host_cores(), "kind": kind,
                "sample": f"{tasks} tasks in {secs:.1f} s: {detail}"}
     line = {
-        "metric": "voted tasks/sec (DMR 4096^2 fp32 matmul, TC vs SIMT variants)",
+        "metric": METRIC,
         "value": total_tasks / t_max,
         "unit": "tasks/s",
         "n_gpus": world,
@@ -466,37 +605,131 @@ def run_hetft_arm(args, rank, world, local):
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic U[1,2) fp32 operands generated on device (no dataset)",
-        "config": {"workload": f"C2: DMR {n}x{n} fp32 matmul, tcgen05-TF32 vs SIMT-FP32 replicas, "
-                               f"HBM checkpoint of inputs, bit-flip faults p={args.fault_prob}/replica, "
-                               f"hf_vote detect-and-rerun", "n": n, "replicas": 2,
-                   "strategy": "hetdmr", "parallelism": f"independent task streams x{world}",
-                   "l2": "operands (3 x 64 MiB) exceed the 126 MB L2; no flush needed"},
+        "config": bench_config(args, world),
         "e2e": {"value": (e2e_steps * world) / t_e2e, "unit": "tasks/s", "steps": e2e_steps,
                 "rounds": e2e_rounds,
                 "note": "own window of max(80, steps) tasks with their own fault draws; the H2D of "
-                        "step i+2 and the D2H of step i-1 overlap step i, PCIe-bound (~2.56 ms/step)",
+                        "step i+2 and the D2H of step i-1 overlap step i (PCIe: 192 MiB per step)",
                 "h2d_bytes_per_step": 2 * nb,
                 "d2h_bytes_per_step": nb},
         "gpu_launches": launches,
         "clocks": clocks,
-        "roofline": {"bound": "fp32-simt", "kernel": "hf_gemm_simt (incl. A^T pre-pass)",
+        "roofline": {"bound": "fp32-simt", "kernel": "hf_gemm_simt (incl. A^T pre-pass), in-task",
                      "achieved": simt_tflops, "peak": ffma_peak, "unit": "TFLOP/s",
                      "frac": (simt_tflops / ffma_peak) if simt_tflops else None, "traffic": traffic,
                      "traffic_unit": "DRAM bytes per launch (ncu --set full, GEMM + A^T pre-pass; "
                                      f"operand bytes 3*{n}^2*4 = {3 * nb})",
                      "peak_source": ffma_src,
-                     "algorithmic": f"2*{n}^3 flop per launch"},
+                     "algorithmic": f"2*{n}^3 flop per launch",
+                     "step_bound": {"simt_alone_ms": 1e3 * flops / (ffma_peak * 1e12),
+                                    "tasks_per_s_at_peak": ffma_peak * 1e12 / flops,
+                                    "frac": (total_tasks / t_max) / world / (ffma_peak * 1e12 / flops)}},
         "rooflines": kern,
-        "replica_ms": {"mm_simt": simt_ns * 1e-6, "mm_tc": tc_ns * 1e-6},
+        "replica_ms": {"mm_simt": simt_ms, "mm_tc": tc_ms, "mm_tc3x": tc3_ms},
         "voter_gbs_in_task": vote_gbs,
-        "tmr": tmr,
+        "dmr": dmr,
+        "c3": c3,
         "detect": detect,
-        "faults": {"injected": stats["injected"], "detected_mismatch_votes": stats["mismatch"],
-                   "votes": stats["votes"], "rounds": stats["rounds"]},
+        "faults": {"injected": stats["injected"], "corrected_votes": stats["corrected"],
+                   "mismatch_votes": stats["mismatch"], "votes": stats["votes"], "rounds": stats["rounds"]},
         "cpu_baseline": cpu,
         "peaks": {"source": peak_src, **peaks},
     }
     print(json.dumps(line), flush=True)
+
+
+def p2p_peak(src_dev: int, dst_dev: int, torch, nbytes: int = 1 << 30):
+    """NVLink P2P roofline denominator, measured: hf_copy of `nbytes` from
+    src_dev's HBM into dst_dev's (the copy kernel on dst_dev pulling peer
+    loads, the voter's access pattern), CUDA-event timed on dst_dev after
+    warm-up; best of 5.  GB/s of NVLink ingress into dst_dev."""
+    from paper_1405_2912_b200 import _lib, kernels
+    _lib.enable_peers()
+    if not _lib.peer_enabled(dst_dev, src_dev):
+        return None
+    src = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{src_dev}")
+    dst = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{dst_dev}")
+    src.fill_(1)
+    torch.cuda.synchronize(src_dev)
+    st = torch.cuda.Stream(device=dst_dev)
+    best = None
+    with torch.cuda.device(dst_dev):
+        for it in range(7):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            kernels.copy(dst, src, stream=st)
+            e1.record(st)
+            st.synchronize()
+            if it >= 2:
+                t = e0.elapsed_time(e1) * 1e-3
+                best = t if best is None else min(best, t)
+    return nbytes / best / 1e9
+
+
+def c3_rate(args, torch, devices=(0, 1, 2)):
+    """BASELINE configs[2]: HetTMR n x n with the three replicas on three
+    distinct GPUs (fleets.b200_replica_fleet_config: SIMT FP32 on GPU 0 with
+    the inputs, tcgen05 TF32 on GPU 1, tcgen05 3xBF16 on GPU 2;
+    Strategy(spread="device")), inputs device-resident on GPU 0 and pulled by
+    the other replicas over NVLink, the K = 3 vote sliced over the three GPUs
+    (each votes a third, loading the other replicas' thirds from their
+    peers), in-place into the SIMT replica.  CUDA-event timed on every GPU's
+    compute stream; the max over the GPUs is the time.  Also reports the
+    sliced vote's per-GPU NVLink ingress rate against a measured P2P peak."""
+    import paper_1405_2912_b200 as hf
+    n = args.n
+    nb = n * n * 4
+    try:
+        cfg = hf.b200_replica_fleet_config(devices=devices)
+        for u in cfg["units"]:
+            u.update({"corrupt_prob": args.fault_prob, "corrupt_mode": "bitflip",
+                      "seed": args.seed * 1_000_003 + u["seed"]})
+        rt = hf.Runtime(hf.load_fleet(cfg), hf.RuntimeConfig(checkpoint_space="ckpt", serial_replicas=True,
+                                                             attempt_limit=64))
+        task = hf.get_workload("matmul").attach(rt, kinds=TMR_KINDS)
+        # one replica per GPU (on a box without three GPUs, devices may repeat:
+        # the one-variant-per-space fleet still forces one replica per space)
+        spread = "device" if len(set(devices)) == len(devices) else "unit"
+        b = TaskStreamBench(args, devices[0], 0, TMR_KINDS, hf.Strategy(hf.StrategyKind.HET_TMR, spread=spread),
+                            built=(hf, rt, task), space="r0mem")
+        rt.executor._trace = b.on_trace
+        b.warm()
+        steps = max(30, args.steps)
+        devs = sorted(set(devices))
+        for d in devs:
+            torch.cuda.synchronize(d)
+        starts, ends = {}, {}
+        for d in devs:
+            starts[d] = torch.cuda.Event(enable_timing=True)
+            starts[d].record(rt.backend.stream(d))
+        b.device_stream(steps, True)
+        for d in devs:
+            ends[d] = torch.cuda.Event(enable_timing=True)
+            ends[d].record(rt.backend.stream(d))
+        for d in devs:
+            torch.cuda.synchronize(d)
+        t = max(starts[d].elapsed_time(ends[d]) for d in devs) * 1e-3
+        st = b.stats
+        votes = sum(st["votes"].values())
+        vote_s = st["vote_ns"] * 1e-9 / votes if votes else None
+        K = 3
+        ingress = (K - 1) / K * nb            # NVLink bytes into each voting GPU per vote
+        peak = p2p_peak(devices[1], devices[0], torch) if len(devs) > 1 else None
+        vote_gbs = ingress / vote_s / 1e9 if vote_s and len(devs) > 1 else None
+        return {"value": steps / t, "unit": "tasks/s", "steps": steps, "ms_per_task": 1e3 * t / steps,
+                "devices": list(devices),
+                "workload": f"HetTMR {n}x{n}, replicas on GPUs {list(devices)} (SIMT / TF32 / 3xBF16), inputs "
+                            f"on GPU {devices[0]} pulled over NVLink, vote sliced over the replica GPUs",
+                "votes": st["votes"], "rounds": st["rounds"],
+                "replica_ms": {k: b.kernel_ms(k) for k in ("mm_simt", "mm_tc", "mm_tc3x")},
+                "vote_us": vote_s * 1e6 if vote_s else None,
+                "nvlink": {"bytes_per_gpu_per_vote": ingress, "achieved_gbs": vote_gbs,
+                           "peak_gbs": peak, "frac": (vote_gbs / peak) if vote_gbs and peak else None,
+                           "peak_source": f"measured: hf_copy GPU{devices[1]}->GPU{devices[0]} 1 GiB pull, "
+                                          "best of 5 (bench.p2p_peak)",
+                           "input_bytes_per_task": 2 * 2 * nb}}
+    except Exception as exc:  # noqa: BLE001 - reported, the headline line still prints
+        return {"error": f"{type(exc).__name__}: {exc}"}
 
 
 def fp32_peak(sm_max_mhz: float):
@@ -638,71 +871,6 @@ def kernel_rooflines(device, n, kernels, torch):
     out["hf_gemm_simt"] = {"bound": "fp32-simt", "achieved": 2 * n ** 3 / t / 1e12, "unit": "TFLOP/s",
                            "us": t * 1e6}
     return out
-
-
-def tmr_rate(device, n, fault_prob, seed, steps, warmup, torch):
-    """North-star headline shape on one GPU: HetTMR of the three diverse
-    variants (tcgen05 TF32, SIMT FP32, tcgen05 3xBF16) on a 4096^2 fp32
-    matmul, device-resident inputs checkpointed into HBM, bit-flip faults at
-    the same per-replica probability, majority vote (K = 3) corrects a single
-    faulty replica.  CUDA-event timed on the runtime's compute stream."""
-    import paper_1405_2912_b200 as hf
-    kinds = ("gpu-tc", "gpu-simt", "gpu-tc3")
-    cfg = hf.gpu_fleet_config(devices=(device,), kinds=kinds)
-    cfg["memory_spaces"].append({"id": f"gpu{device}ckpt", "device": device, "label": "HBM checkpoint reserve"})
-    for i, u in enumerate(cfg["units"]):
-        u.update({"corrupt_prob": fault_prob, "corrupt_mode": "bitflip", "seed": seed * 1_000_003 + i * 101 + 31})
-    rt = hf.Runtime(hf.load_fleet(cfg), hf.RuntimeConfig(checkpoint_space=f"gpu{device}ckpt",
-                                                         serial_replicas=True, attempt_limit=64))
-    task = hf.get_workload("matmul").attach(rt, kinds=kinds)
-    space = f"gpu{device}mem"
-    nb = n * n * 4
-    rt.reserve(space, nb, 24)
-    g = torch.Generator(device=f"cuda:{device}")
-    g.manual_seed(seed * 7919 + 5)
-    A = (torch.rand(n * n, device=f"cuda:{device}", generator=g) + 1).view(torch.uint8)
-    B = (torch.rand(n * n, device=f"cuda:{device}", generator=g) + 1).view(torch.uint8)
-    C0 = torch.zeros(nb, dtype=torch.uint8, device=f"cuda:{device}")
-    strat = hf.Strategy(hf.StrategyKind.HET_TMR)
-    votes, rounds = {}, 0
-
-    def go(k, recording):
-        nonlocal rounds
-        queue = []
-        with rt.task_stream(depth=1) as ts:
-            for _ in range(k):
-                areas = tuple(rt.register_device_data(x, n * n, hf.ValueType.FLOAT32, m, space)
-                              for x, m in ((A, "r"), (B, "r"), (C0, "w")))
-                queue.append((ts.submit(task, dict(zip("ABC", areas), n=n), strat), areas))
-                while queue and queue[0][0].success:
-                    rep, ar = queue.pop(0)
-                    if recording:
-                        rounds += rep.rounds
-                        for v in rep.votes:
-                            votes[v] = votes.get(v, 0) + 1
-                    for x in ar:
-                        rt.release(x)
-        for rep, ar in queue:
-            if recording:
-                rounds += rep.rounds
-                for v in rep.votes:
-                    votes[v] = votes.get(v, 0) + 1
-            for x in ar:
-                rt.release(x)
-
-    go(max(3, warmup), False)
-    st = rt.backend.stream(device)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(st)
-    go(steps, True)
-    e1.record(st)
-    torch.cuda.synchronize()
-    t = e0.elapsed_time(e1) * 1e-3
-    return {"value": steps / t, "unit": "tasks/s", "ms_per_task": 1e3 * t / steps, "steps": steps,
-            "workload": f"HetTMR {n}x{n} fp32 matmul (tcgen05 TF32 + SIMT FP32 + tcgen05 3xBF16 replicas "
-                        f"on 1 GPU), HBM checkpoint of inputs, bit flips p={fault_prob}/replica, K=3 majority vote",
-            "votes": votes, "rounds": rounds}
 
 
 def main():

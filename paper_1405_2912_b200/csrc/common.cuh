@@ -142,6 +142,13 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 // PDL: let the stream's next grid start launching.
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Load rule for source buffers (replicas, copy sources, snapshots): a
+// buffer the kernel only reads is read-only for the kernel's lifetime — its
+// producers (another stream, another GPU, the host) are ordered before the
+// launch by events — so it is loaded with ld.global.nc whether it is local
+// HBM, a peer GPU's memory (NVLink) or mapped pinned host memory (UVA).  A
+// buffer the same kernel also stores into (the in-place vote target) is
+// loaded coherently with ld_stream_rw.
 // 128-bit streaming load that does not allocate in L1 (read-once data).
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
     uint4 r;
@@ -151,11 +158,11 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
     return r;
 }
 
-// 128-bit coherent load (peer / host mapped memory may be written by others;
-// also used where the non-coherent path is not allowed).
-__device__ __forceinline__ uint4 ld_plain(const uint4* p) {
+// 128-bit coherent streaming load (no .nc, no L1 allocation): for a buffer
+// the kernel itself writes (in-place vote target).
+__device__ __forceinline__ uint4 ld_stream_rw(const uint4* p) {
     uint4 r;
-    asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+    asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                  : "l"(p));
     return r;

@@ -39,7 +39,7 @@ __device__ __forceinline__ unsigned long long mix_vec(const uint4& v, unsigned l
            mix_word(v.z, j0 + 2) + mix_word(v.w, j0 + 3);
 }
 
-template <bool kStore, bool kSum, bool kPeerSrc>
+template <bool kStore, bool kSum>
 __global__ void __launch_bounds__(256) stream_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src,
                                                      long long nvec, const uint8_t* __restrict__ src_b,
                                                      uint8_t* __restrict__ dst_b, long long nbytes,
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(256) stream_kernel(uint4* __restrict__ dst, co
     for (; j + (U - 1) * gs < nvec; j += U * gs) {
         uint4 v[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) v[u] = kPeerSrc ? ld_plain(src + j + u * gs) : ld_stream(src + j + u * gs);
+        for (int u = 0; u < U; ++u) v[u] = ld_stream(src + j + u * gs);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if constexpr (kStore) st_stream(dst + j + u * gs, v[u]);
@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(256) stream_kernel(uint4* __restrict__ dst, co
         }
     }
     for (; j < nvec; j += gs) {
-        uint4 v = kPeerSrc ? ld_plain(src + j) : ld_stream(src + j);
+        uint4 v = ld_stream(src + j);
         if constexpr (kStore) st_stream(dst + j, v);
         if constexpr (kSum) acc += mix_vec(v, static_cast<unsigned long long>(j) * 4);
     }
@@ -107,7 +107,11 @@ static int grid_for(long long work, int device) {
 // Launch the streaming kernel; nvec = 16B vectors when both pointers are 16B
 // aligned, else 0 (byte path).
 static int launch_stream(void* dst, const void* src, long long nbytes, unsigned long long* sum,
-                         bool peer_src, int device, cudaStream_t st) {
+                         int device, cudaStream_t st) {
+    // Source loads are ld.global.nc whether `src` is local HBM, a peer GPU's
+    // memory or mapped host memory: the source is read-only for the kernel's
+    // lifetime (its producers are ordered before this launch by stream
+    // events), which is all .nc requires (see ld_stream in common.cuh).
     bool aligned = reinterpret_cast<uintptr_t>(src) % 16 == 0 &&
                    (dst == nullptr || reinterpret_cast<uintptr_t>(dst) % 16 == 0);
     long long nvec = aligned ? nbytes / 16 : 0;
@@ -118,14 +122,11 @@ static int launch_stream(void* dst, const void* src, long long nbytes, unsigned 
     auto sb = static_cast<const uint8_t*>(src);
     auto db = static_cast<uint8_t*>(dst);
     if (dst && sum) {
-        if (peer_src) HF_CUDA_CHECK(launch_pdl(stream_kernel<true, true, true>, dim3(grid), dim3(256), 0, st, d4, s4, nvec, sb, db, nbytes, sum));
-        else HF_CUDA_CHECK(launch_pdl(stream_kernel<true, true, false>, dim3(grid), dim3(256), 0, st, d4, s4, nvec, sb, db, nbytes, sum));
+        HF_CUDA_CHECK(launch_pdl(stream_kernel<true, true>, dim3(grid), dim3(256), 0, st, d4, s4, nvec, sb, db, nbytes, sum));
     } else if (dst) {
-        if (peer_src) HF_CUDA_CHECK(launch_pdl(stream_kernel<true, false, true>, dim3(grid), dim3(256), 0, st, d4, s4, nvec, sb, db, nbytes, sum));
-        else HF_CUDA_CHECK(launch_pdl(stream_kernel<true, false, false>, dim3(grid), dim3(256), 0, st, d4, s4, nvec, sb, db, nbytes, sum));
+        HF_CUDA_CHECK(launch_pdl(stream_kernel<true, false>, dim3(grid), dim3(256), 0, st, d4, s4, nvec, sb, db, nbytes, sum));
     } else {
-        if (peer_src) HF_CUDA_CHECK(launch_pdl(stream_kernel<false, true, true>, dim3(grid), dim3(256), 0, st, d4, s4, nvec, sb, db, nbytes, sum));
-        else HF_CUDA_CHECK(launch_pdl(stream_kernel<false, true, false>, dim3(grid), dim3(256), 0, st, d4, s4, nvec, sb, db, nbytes, sum));
+        HF_CUDA_CHECK(launch_pdl(stream_kernel<false, true>, dim3(grid), dim3(256), 0, st, d4, s4, nvec, sb, db, nbytes, sum));
     }
     HF_CHECK_LAUNCH();
     return HF_OK;
@@ -158,13 +159,13 @@ static void release(int device, const SumSlot& s) {
     g_slots[device].push_back(s);
 }
 
-static int checksum_impl(void* dst, const void* src, long long nbytes, uint64_t* out, bool peer_src,
+static int checksum_impl(void* dst, const void* src, long long nbytes, uint64_t* out,
                          int device, cudaStream_t st) {
     SumSlot s;
     int rc = acquire(device, s);
     if (rc) return rc;
     HF_CUDA_CHECK(cudaMemsetAsync(s.d, 0, sizeof(unsigned long long), st));
-    rc = launch_stream(dst, src, nbytes, s.d, peer_src, device, st);
+    rc = launch_stream(dst, src, nbytes, s.d, device, st);
     if (rc) return rc;
     HF_CUDA_CHECK(cudaMemcpyAsync(s.h, s.d, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     HF_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -173,22 +174,9 @@ static int checksum_impl(void* dst, const void* src, long long nbytes, uint64_t*
     return HF_OK;
 }
 
-static int device_of(const void* p, int* dev) {
-    cudaPointerAttributes a;
-    cudaError_t e = cudaPointerGetAttributes(&a, p);
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        *dev = -1;
-        return HF_OK;
-    }
-    *dev = a.type == cudaMemoryTypeDevice ? a.device : -1;
-    return HF_OK;
-}
-
 static const int kRegistered = register_kernels(
-    {(const void*)stream_kernel<true, true, true>, (const void*)stream_kernel<true, true, false>,
-     (const void*)stream_kernel<true, false, true>, (const void*)stream_kernel<true, false, false>,
-     (const void*)stream_kernel<false, true, true>, (const void*)stream_kernel<false, true, false>});
+    {(const void*)stream_kernel<true, true>, (const void*)stream_kernel<true, false>,
+     (const void*)stream_kernel<false, true>});
 
 }  // namespace hf
 
@@ -203,7 +191,7 @@ int hf_copy(void* dst, int dst_dev, const void* src, int src_dev, int64_t nbytes
         if (dst_dev == src_dev || hf_peer_enabled(dst_dev, src_dev)) {
             hf::DeviceGuard g(dst_dev);
             HF_REQUIRE(g.ok, "hf_copy: cannot select device %d", dst_dev);
-            return hf::launch_stream(dst, src, nbytes, nullptr, dst_dev != src_dev, dst_dev, st);
+            return hf::launch_stream(dst, src, nbytes, nullptr, dst_dev, st);
         }
         HF_CUDA_CHECK(cudaMemcpyPeerAsync(dst, dst_dev, src, src_dev, static_cast<size_t>(nbytes), st));
         return HF_OK;
@@ -237,8 +225,8 @@ int hf_checkpoint(void* ckpt, const void* buf, int64_t nbytes, uint64_t* checksu
     cudaStream_t st = hf::as_stream(stream);
     // The snapshot may live on a peer GPU: the kernel runs on `device` and
     // stores through the peer pointer (NVLink write).
-    if (checksum) return hf::checksum_impl(ckpt, buf, nbytes, checksum, false, device, st);
-    return hf::launch_stream(ckpt, buf, nbytes, nullptr, false, device, st);
+    if (checksum) return hf::checksum_impl(ckpt, buf, nbytes, checksum, device, st);
+    return hf::launch_stream(ckpt, buf, nbytes, nullptr, device, st);
 }
 
 int hf_restore(void* buf, const void* ckpt, int64_t nbytes, const uint64_t* expect, int device,
@@ -250,21 +238,19 @@ int hf_restore(void* buf, const void* ckpt, int64_t nbytes, const uint64_t* expe
     hf::DeviceGuard g(device);
     HF_REQUIRE(g.ok, "hf_restore: cannot select device %d", device);
     cudaStream_t st = hf::as_stream(stream);
-    int src_dev = -1;
-    hf::device_of(ckpt, &src_dev);
-    bool peer = src_dev >= 0 && src_dev != device;
     if (expect) {
+        // verify first, then write: a snapshot that fails its checksum never
+        // reaches `buf` (one extra read pass of the snapshot)
         uint64_t got = 0;
-        int rc = hf::checksum_impl(buf, ckpt, nbytes, &got, peer, device, st);
+        int rc = hf::checksum_impl(nullptr, ckpt, nbytes, &got, device, st);
         if (rc) return rc;
         if (got != *expect) {
-            hf::set_error("hf_restore: checksum mismatch (expected %016llx, got %016llx)",
+            hf::set_error("hf_restore: checksum mismatch (expected %016llx, got %016llx); buffer left untouched",
                           static_cast<unsigned long long>(*expect), static_cast<unsigned long long>(got));
             return HF_ECHECKSUM;
         }
-        return HF_OK;
     }
-    return hf::launch_stream(buf, ckpt, nbytes, nullptr, peer, device, st);
+    return hf::launch_stream(buf, ckpt, nbytes, nullptr, device, st);
 }
 
 int hf_checksum(const void* buf, int64_t nbytes, uint64_t* out, int device, void* stream) {
@@ -278,10 +264,7 @@ int hf_checksum(const void* buf, int64_t nbytes, uint64_t* out, int device, void
     HF_REQUIRE(buf != nullptr, "hf_checksum: NULL buffer");
     hf::DeviceGuard g(device);
     HF_REQUIRE(g.ok, "hf_checksum: cannot select device %d", device);
-    int src_dev = -1;
-    hf::device_of(buf, &src_dev);
-    return hf::checksum_impl(nullptr, buf, nbytes, out, src_dev >= 0 && src_dev != device, device,
-                             hf::as_stream(stream));
+    return hf::checksum_impl(nullptr, buf, nbytes, out, device, hf::as_stream(stream));
 }
 
 }  // extern "C"

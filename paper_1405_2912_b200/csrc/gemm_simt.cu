@@ -4,7 +4,8 @@
 // OpenMP/CUDA variants (§IV-D; attached through the kernel-variant
 // slot of /root/reference/pkg/src/hetrt/api.py:131-138).  It never touches the
 // tensor cores, accumulates every output in fp32 in ascending k order with
-// fused multiply-add, and so fails independently of the tcgen05 variant.
+// fused multiply-add (in chunks of 512 products summed blockwise, see
+// sgemm_128x128), and so fails independently of the tcgen05 variant.
 //
 // Fast path (M%128 == N%128 == 0, K%32 == 0, 16B-aligned): A is transposed
 // once by a tiled pre-pass (~2|A| bytes, ~1% of the GEMM) so both operands
@@ -35,6 +36,11 @@ __device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
 __device__ __forceinline__ void ffma2(unsigned long long& d, unsigned long long a, unsigned long long b) {
     asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
 }
+__device__ __forceinline__ unsigned long long fadd2(unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
@@ -53,12 +59,25 @@ __device__ __forceinline__ void cp_async_wait() {
 // ring without staging registers; fragments for k+1 are read from smem
 // while k is multiplied.  <= 128 registers: two CTAs (16 warps) per SM hide
 // each other's barrier and latency stalls.
+//
+// Blocked accumulation (CH > 0, the default): the fp32 FMA chain of an
+// output runs over CH k-tiles (CH*16 products) only; the chunk's sum is then
+// added (one rounding) into a running total that lives in shared memory, 64
+// floats per thread laid out [16][256] x 16 B (conflict-free 128-bit
+// accesses), and the register accumulators restart at zero — the blocked
+// summation an optimised CPU sgemm does.  At 4096^2 the max relative error
+// against the binary64 product is 7.1e-7 (numpy/OpenBLAS fp32, the
+// reference body's arithmetic: 5.5e-7) instead of 5.4e-6 for one 4096-long
+// chain, for 64 KB more smem per CTA (112 KB: still two CTAs per SM) and
+// ~5% of kernel time.  CH = 0: one chain in ascending k (A/B only).
+template <int CH>
 __global__ void __launch_bounds__(256, 2)
 sgemm_128x128(const float* __restrict__ At, const float* __restrict__ B, float* __restrict__ C,
               int M, int N, int K, int group) {
     extern __shared__ __align__(16) float sm[];
     float* As = sm;                                   // [S][SB_K][SB_M]
     float* Bs = sm + S_STAGES * SB_K * SB_M;          // [S][SB_K][SB_N]
+    ulonglong2* Tot = reinterpret_cast<ulonglong2*>(Bs + S_STAGES * SB_K * SB_N);   // [16][256]
 
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;
@@ -102,6 +121,46 @@ sgemm_128x128(const float* __restrict__ At, const float* __restrict__ B, float* 
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = 0ull;
 
+    if constexpr (CH > 0) {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) Tot[q * 256 + t] = make_ulonglong2(0ull, 0ull);
+    }
+    // running total += chunk sum (acc pair (i, j) <-> Tot[q = 2i + j/2], half
+    // j&1), then the chain restarts at zero.  Written in asm that updates
+    // the accumulators in place, behind a branch inside the asm, and called
+    // from the single k-tile loop: a C++ restart at zero (or a nested chunk
+    // loop) gave every accumulator a second definition, ptxas assigned them
+    // different registers and the loop back-edge grew ~32 MOVs per k-tile
+    // (+4.5% time).  `go` is warp-uniform.
+    const uint32_t tot_s = static_cast<uint32_t>(__cvta_generic_to_shared(Tot + t));
+    auto flush = [&](uint32_t go) {
+#pragma unroll
+        for (int i = 0; i < 8; i += 2)
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t.reg .b64 t0, t1, t2, t3, t4, t5, t6, t7;\n\t"
+                "setp.eq.u32 p, %8, 0;\n\t"
+                "@p bra.uni FLUSH_SKIP%=;\n\t"
+                "ld.shared.v2.b64 {t0, t1}, [%9];\n\t"
+                "ld.shared.v2.b64 {t2, t3}, [%9+4096];\n\t"
+                "ld.shared.v2.b64 {t4, t5}, [%9+8192];\n\t"
+                "ld.shared.v2.b64 {t6, t7}, [%9+12288];\n\t"
+                "add.rn.f32x2 t0, t0, %0;\n\tadd.rn.f32x2 t1, t1, %1;\n\t"
+                "add.rn.f32x2 t2, t2, %2;\n\tadd.rn.f32x2 t3, t3, %3;\n\t"
+                "add.rn.f32x2 t4, t4, %4;\n\tadd.rn.f32x2 t5, t5, %5;\n\t"
+                "add.rn.f32x2 t6, t6, %6;\n\tadd.rn.f32x2 t7, t7, %7;\n\t"
+                "st.shared.v2.b64 [%9], {t0, t1};\n\t"
+                "st.shared.v2.b64 [%9+4096], {t2, t3};\n\t"
+                "st.shared.v2.b64 [%9+8192], {t4, t5};\n\t"
+                "st.shared.v2.b64 [%9+12288], {t6, t7};\n\t"
+                "mov.b64 %0, 0;\n\tmov.b64 %1, 0;\n\tmov.b64 %2, 0;\n\tmov.b64 %3, 0;\n\t"
+                "mov.b64 %4, 0;\n\tmov.b64 %5, 0;\n\tmov.b64 %6, 0;\n\tmov.b64 %7, 0;\n\t"
+                "FLUSH_SKIP%=:\n\t}"
+                : "+l"(acc[i][0]), "+l"(acc[i][1]), "+l"(acc[i][2]), "+l"(acc[i][3]),
+                  "+l"(acc[i + 1][0]), "+l"(acc[i + 1][1]), "+l"(acc[i + 1][2]), "+l"(acc[i + 1][3])
+                : "r"(go), "r"(tot_s + static_cast<uint32_t>(2 * i * 256 * 16))
+                : "memory");
+    };
+
     const int nk = K / SB_K;
     pdl_wait();     // launched with PDL behind the A^T pre-pass: At is complete from here
 #pragma unroll
@@ -110,7 +169,7 @@ sgemm_128x128(const float* __restrict__ At, const float* __restrict__ B, float* 
         cp_async_commit();
     }
 
-    for (int kt = 0; kt < nk; ++kt) {
+    auto ktile = [&](int kt) {
         cp_async_wait<S_STAGES - 2>();
         __syncthreads();
         {
@@ -146,8 +205,22 @@ sgemm_128x128(const float* __restrict__ At, const float* __restrict__ B, float* 
                 for (int j = 0; j < 4; ++j) ffma2(acc[i][j], ai, b[j]);
             }
         }
+    };
+    for (int kt = 0; kt < nk; ++kt) {
+        ktile(kt);
+        if constexpr (CH > 0) flush(static_cast<uint32_t>((kt + 1) % CH == 0 || kt + 1 == nk));
     }
     cp_async_wait<0>();
+    if constexpr (CH > 0) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const ulonglong2 v = Tot[(2 * i + h) * 256 + t];
+                acc[i][2 * h] = v.x;
+                acc[i][2 * h + 1] = v.y;
+            }
+    }
 
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -158,7 +231,13 @@ sgemm_128x128(const float* __restrict__ At, const float* __restrict__ B, float* 
     }
 }
 
-constexpr int SGEMM_SMEM = S_STAGES * SB_K * (SB_M + SB_N) * 4;
+// k-tiles per FMA chain: 32 (512 products).  At 4096^2 (tools/simt_ab.py,
+// profiles/r02_simt_ab6.jsonl): max rel err 7.1e-7 (numpy fp32 5.5e-7; one
+// 4096-long chain 5.4e-6), 2.346 ms vs 2.220 ms for the chain kernel.  CH 8:
+// 4.5e-7 but the flushes' smem traffic adds another 2%; CH 64: 1.3e-6, 2.336 ms.
+constexpr int SGEMM_CH = 32;
+constexpr int SGEMM_SMEM_RING = S_STAGES * SB_K * (SB_M + SB_N) * 4;   // 48 KB
+constexpr int SGEMM_SMEM = SGEMM_SMEM_RING + 16 * 256 * 16;            // + 64 KB running totals
 // Co-scheduled with the tensor-core replica (HF_GEMM_COSCHEDULE): each CTA
 // reserves 100 KB although it uses 48 KB.  Two SIMT CTAs still fit an SM,
 // and when one retires the space it frees takes one TC CTA (2-stage shape,
@@ -167,7 +246,10 @@ constexpr int SGEMM_SMEM = S_STAGES * SB_K * (SB_M + SB_N) * 4;
 // 4096^2, SIMT + TC replicas on two streams: 2.33 ms vs 2.45 ms with the
 // 48 KB reservation (tools/cosched_bench.py); at <= 96 KB the TC CTAs are
 // not placed until the SIMT grid drains.
-constexpr int SGEMM_SMEM_COSCHED = 100000;
+// With the 112 KB of the blocked-accumulation kernel the reservation is its
+// own footprint: two CTAs use 226 KB of the SM's 228 KB, and one retiring
+// frees room for one TC CTA exactly as the 100 KB reservation did.
+constexpr int SGEMM_SMEM_COSCHED = SGEMM_SMEM > 100000 ? SGEMM_SMEM : 100000;
 constexpr int SGEMM_SMEM_MAX = 227 * 1024;
 
 // A (M x K) -> At (K x M), 32x32 tiles through padded smem.
@@ -205,19 +287,26 @@ sgemm_generic(const float* __restrict__ A, const float* __restrict__ B, float* _
 }
 
 static const int kRegistered =
-    register_kernels({(const void*)sgemm_128x128, (const void*)transpose_a, (const void*)sgemm_generic});
+    register_kernels({(const void*)sgemm_128x128<SGEMM_CH>, (const void*)sgemm_128x128<0>,
+                      (const void*)transpose_a, (const void*)sgemm_generic});
 
 }  // namespace hf
 
 namespace hf {
 // Co-scheduling smem reservation per SIMT CTA (HF_SGEMM_COSCHED_SMEM bytes,
 // experiments only; default SGEMM_SMEM_COSCHED).
+static bool sgemm_chain() {
+    static const int on = getenv("HF_SGEMM_CHAIN") != nullptr && getenv("HF_SGEMM_CHAIN")[0] == '1';
+    return on != 0;
+}
+
 static int sgemm_cosched_smem() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("HF_SGEMM_COSCHED_SMEM");
         int x = e ? atoi(e) : SGEMM_SMEM_COSCHED;
-        v = x >= SGEMM_SMEM && x <= SGEMM_SMEM_MAX ? x : SGEMM_SMEM_COSCHED;
+        v = x >= SGEMM_SMEM_RING && x <= SGEMM_SMEM_MAX ? x : SGEMM_SMEM_COSCHED;
+        if (v < SGEMM_SMEM && !sgemm_chain()) v = SGEMM_SMEM;
     }
     return v;
 }
@@ -260,29 +349,30 @@ extern "C" int hf_gemm_simt(const float* A, const float* B, float* C, int M, int
     if (aligned && M % hf::SB_M == 0 && N % hf::SB_N == 0 && K % 32 == 0) {
         static bool attr[64] = {false};
         if (!attr[device]) {
-            HF_CUDA_CHECK(cudaFuncSetAttribute(hf::sgemm_128x128, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            HF_CUDA_CHECK(cudaFuncSetAttribute(hf::sgemm_128x128<hf::SGEMM_CH>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, hf::SGEMM_SMEM_MAX));
+            HF_CUDA_CHECK(cudaFuncSetAttribute(hf::sgemm_128x128<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                hf::SGEMM_SMEM_MAX));
             attr[device] = true;
         }
-        float* At = static_cast<float*>(hf::stream_scratch(device, st, 2, static_cast<size_t>(M) * K * sizeof(float)));
-        if (!At) {
-            hf::set_error("hf_gemm_simt: cannot allocate the A^T scratch");
-            return HF_ECUDA;
-        }
+        // HF_SGEMM_CHAIN=1 (A/B only): one fp32 chain over all of K, 48 KB
+        const bool chain = hf::sgemm_chain();
+        auto kern = chain ? hf::sgemm_128x128<0> : hf::sgemm_128x128<hf::SGEMM_CH>;
         // Co-scheduled: the A^T pre-pass runs on the device's greatest-priority
         // side stream, ahead of the tensor-core replica's pre-pass (level 1),
         // so this GEMM's grid is pending before the TC GEMM's and, launched on
         // the executor's higher-priority lead stream, is dispatched first; the
         // TC CTAs then fill its last wave.
         int tiles = (M / hf::SB_M) * (N / hf::SB_N);
-        const int smem = (mode & HF_GEMM_COSCHEDULE) ? hf::sgemm_cosched_smem() : hf::SGEMM_SMEM;
+        int smem = (mode & HF_GEMM_COSCHEDULE) ? hf::sgemm_cosched_smem() : hf::SGEMM_SMEM;
+        if (chain && !(mode & HF_GEMM_COSCHEDULE)) smem = hf::SGEMM_SMEM_RING;
         if (hf::simt_pdl()) {
             // HF_SIMT_PDL=1: A^T pre-pass and GEMM on the caller's stream, the
             // GEMM launched with PDL (no launch gap after the pre-pass).  Off
             // by default: co-scheduled with a TC replica the TC GEMM then got
             // SMs at the start of the SIMT grid, 2.46 -> 2.49 ms per DMR round
             HF_CUDA_CHECK(hf::launch_pdl(hf::transpose_a, dim3(K / 32, M / 32), dim3(256), 0, st, A, At, M, K));
-            HF_CUDA_CHECK(hf::launch_pdl(hf::sgemm_128x128, dim3(tiles), dim3(256), smem, st, At, B, C, M, N, K,
+            HF_CUDA_CHECK(hf::launch_pdl(kern, dim3(tiles), dim3(256), smem, st, At, B, C, M, N, K,
                                          hf::sgemm_group()));
         } else if (hf::side_prepass()) {
             // default: the pre-pass on the device's greatest-priority side
@@ -294,7 +384,7 @@ extern "C" int hf_gemm_simt(const float* A, const float* B, float* C, int M, int
             HF_CUDA_CHECK(hf::begin_side_launch(side, st, &ps));
             hf::transpose_a<<<dim3(K / 32, M / 32), 256, 0, ps>>>(A, At, M, K);
             HF_CUDA_CHECK(hf::end_side_launch(side, st));
-            hf::sgemm_128x128<<<tiles, 256, smem, st>>>(At, B, C, M, N, K, hf::sgemm_group());
+            kern<<<tiles, 256, smem, st>>>(At, B, C, M, N, K, hf::sgemm_group());
         } else {
             // HF_SIMT_SIDE_PREPASS=0: pre-pass and GEMM in stream order on the
             // caller's stream (no event gap).  Co-scheduled, the TC pre-pass
@@ -302,7 +392,7 @@ extern "C" int hf_gemm_simt(const float* A, const float* B, float* C, int M, int
             // the SIMT grid, even with the lead stream at the greatest priority
             // (2.44 -> 2.57 ms per DMR round)
             hf::transpose_a<<<dim3(K / 32, M / 32), 256, 0, st>>>(A, At, M, K);
-            hf::sgemm_128x128<<<tiles, 256, smem, st>>>(At, B, C, M, N, K, hf::sgemm_group());
+            kern<<<tiles, 256, smem, st>>>(At, B, C, M, N, K, hf::sgemm_group());
         }
     } else {
         dim3 grid((N + 15) / 16, (M + 15) / 16);

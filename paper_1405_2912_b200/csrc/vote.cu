@@ -16,8 +16,9 @@
 //   winner      = argmin mismatch (ties -> lowest r)
 //
 // Design (B200): one pass over all K replicas, 128-bit streaming loads
-// (ld.global.nc.L1::no_allocate; peer-device pointers are loaded directly
-// over NVLink), counts kept in registers, warp reduction with
+// (ld.global.nc.L1::no_allocate for every replica the kernel does not write,
+// local, peer-GPU over NVLink or mapped host memory alike; the in-place
+// target is loaded coherently, see common.cuh), counts kept in registers, warp reduction with
 // __reduce_add_sync, ballot-gated first-divergence min, one atomic per block,
 // and a last-block epilogue that finalises the result and re-arms the
 // workspace so back-to-back votes need a single launch each.
@@ -321,7 +322,9 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
         for (int u = 0; u < UNROLL; ++u)
 #pragma unroll
             for (int r = 0; r < K; ++r)
-                v[u][r] = ld_stream(reinterpret_cast<const uint4*>(p.rep[r]) + (j + u * gstride));
+                v[u][r] = (r == 0 && p.in_place)
+                              ? ld_stream_rw(reinterpret_cast<const uint4*>(p.rep[r]) + (j + u * gstride))
+                              : ld_stream(reinterpret_cast<const uint4*>(p.rep[r]) + (j + u * gstride));
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u) {
             const long long vj = j + u * gstride;
@@ -365,7 +368,9 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
     for (; j < p.nvec; j += gstride) {
         uint4 v[K];
 #pragma unroll
-        for (int r = 0; r < K; ++r) v[r] = ld_stream(reinterpret_cast<const uint4*>(p.rep[r]) + j);
+        for (int r = 0; r < K; ++r)
+            v[r] = (r == 0 && p.in_place) ? ld_stream_rw(reinterpret_cast<const uint4*>(p.rep[r]) + j)
+                                          : ld_stream(reinterpret_cast<const uint4*>(p.rep[r]) + j);
         T o[PV];
         bool changed = false;
 #pragma unroll
@@ -386,7 +391,9 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
     for (long long i = p.nvec * PV + gtid; i < p.n; i += gstride) {
         T x[K];
 #pragma unroll
-        for (int r = 0; r < K; ++r) x[r] = __ldg(reinterpret_cast<const T*>(p.rep[r]) + i);
+        for (int r = 0; r < K; ++r)
+            x[r] = (r == 0 && p.in_place) ? reinterpret_cast<const volatile T*>(p.rep[r])[i]
+                                          : __ldg(reinterpret_cast<const T*>(p.rep[r]) + i);
         T o = vote_elem<DT, K>(x, p, acc, static_cast<unsigned long long>(i));
         if (p.voted != nullptr && (!p.in_place || o != x[0])) reinterpret_cast<T*>(p.voted)[i] = o;
     }

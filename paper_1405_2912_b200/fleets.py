@@ -53,6 +53,30 @@ def b200_fleet_config() -> dict:
     return cfg
 
 
+def b200_replica_fleet_config(devices=(0, 1, 2), kinds=("gpu-simt", "gpu-tc", "gpu-tc3"),
+                              checkpoint_device: int = None) -> dict:
+    """BASELINE configs[2]: one variant kind per GPU — replica i's kernel
+    kind runs only on GPU devices[i] (unit "r<i>.<kind>" in space "r<i>mem"),
+    so a heterogeneous strategy (distinct kernels) necessarily places its
+    replicas on distinct GPUs.  The SIMT variant, the long pole of a round,
+    sits on devices[0] next to the inputs; the tensor-core variants pull the
+    inputs over NVLink and finish long before it.  Optional HBM checkpoint
+    space "ckpt" on `checkpoint_device` (default devices[0]).  `devices` may
+    repeat an ordinal: (0, 0, 0) keeps the per-replica spaces and the copies
+    between them on one GPU (the code path of this preset on a 1-GPU box)."""
+    if len(devices) != len(kinds):
+        raise ConfigError(f"b200 replica fleet: {len(devices)} devices for {len(kinds)} kinds")
+    spaces = [{"id": "host", "label": "pinned host RAM", "host": True}]
+    units = []
+    for i, (d, kind) in enumerate(zip(devices, kinds)):
+        spaces.append({"id": f"r{i}mem", "device": int(d), "label": f"replica {i} HBM (GPU {d})"})
+        units.append({"id": f"r{i}.{kind.split('-', 1)[-1]}", "kind": kind, "memory_space": f"r{i}mem",
+                      "timing": "measured", "seed": 2000 + 17 * i})
+    cd = devices[0] if checkpoint_device is None else checkpoint_device
+    spaces.append({"id": "ckpt", "device": int(cd), "label": f"HBM checkpoint reserve (GPU {cd})"})
+    return {"memory_spaces": spaces, "units": units, "default_ns_per_byte": 0.0}
+
+
 def b200_multi_fleet_config(n_gpus: int) -> dict:
     """n B200s, one memory space each; the same three kinds on every GPU."""
     return gpu_fleet_config(devices=tuple(range(n_gpus)), kinds=("gpu-tc", "gpu-simt", "gpu-tc3"))
@@ -63,6 +87,7 @@ BUILTIN_FLEETS = {
     "pathfinder": pathfinder_fleet_config,
     "b200": b200_fleet_config,
     **{f"b200x{n}": (lambda n=n: b200_multi_fleet_config(n)) for n in (2, 3, 4, 8)},
+    "b200-replicas3": b200_replica_fleet_config,
 }
 
 

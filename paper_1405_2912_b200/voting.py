@@ -15,6 +15,7 @@ voter profile (hf_vote: ~launch + sync latency, per byte 1/HBM rate).
 
 from __future__ import annotations
 
+import copy
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
@@ -160,43 +161,60 @@ def compare(result_a: dict, result_b: dict, config: VoterConfig, backend=None) -
 
 
 def vote_buffers_start(backend, areas: Sequence[tuple], rel_tols: Sequence[float], ulp: Optional[int] = None,
-                       device: Optional[int] = None, in_place: bool = True) -> list:
+                       device: Optional[int] = None, in_place: bool = True,
+                       order: Optional[Sequence[int]] = None) -> list:
     """Launch a K-way vote per output area without waiting.
 
     areas: (area id, [K buffers], value type, width); voted in sorted area
-    order (reference rule).  With in_place the voted output is written over
-    replica 0's buffer (the kernel only stores elements whose voted value
-    differs from replica 0), so committing replica 0's handles commits the
-    voted result."""
+    order (reference rule).  order: the replica order the voter sees
+    (default 0..K-1).  Appendix A's voted value is the lowest majority
+    replica *in this order*, so the caller puts its preferred replica first;
+    counts, winner and first-divergence values come back in slot order.
+    With in_place the voted output is written over the first replica of
+    `order` (the kernel only stores elements whose voted value differs from
+    it), so committing that replica's handles commits the voted result."""
     areas = sorted(areas, key=lambda a: a[0])
     K = len(areas[0][1]) if areas else 0
+    order = list(range(K)) if order is None else list(order)
+    if sorted(order) != list(range(K)):
+        raise DispatchError(f"replica order {order} is not a permutation of 0..{K - 1}")
     pending = []
     for area, bufs, vt, width in areas:
         if len(bufs) != K:
             raise DispatchError(f"area {area!r}: {len(bufs)} replicas, expected {K}")
+        seen = [bufs[i] for i in order]
         ulps = None if ulp is None or vt.numpy_dtype is None else [ulp] * K
-        h = backend.vote_start(bufs, vt, width, list(rel_tols), ulps,
-                               voted=bufs[0] if (in_place and K >= 3) else None, device=device)
-        pending.append((area, bufs, vt, width, h))
+        h = backend.vote_start(seen, vt, width, [rel_tols[i] for i in order], ulps,
+                               voted=seen[0] if (in_place and K >= 3) else None, device=device)
+        pending.append((area, bufs, vt, width, h, order))
     return pending
 
 
 def vote_buffers_finish(backend, pending: list) -> VoteOutcome:
-    """Wait for the votes of vote_buffers_start and combine the areas."""
+    """Wait for the votes of vote_buffers_start and combine the areas (all
+    per-replica results in slot order)."""
     K = len(pending[0][1]) if pending else 0
     total = [0] * K
     unresolved = 0
     first = None
     per_area = {}
     vote_ns = 0
-    for area, bufs, vt, width, h in pending:
+    for area, bufs, vt, width, h, order in pending:
         res, ns = h.wait()
         vote_ns += ns
+        if order != list(range(K)):
+            mism = [0] * K
+            for j, r in enumerate(order):
+                mism[r] = res.mismatch[j]
+            res = copy.copy(res)
+            res.mismatch = mism
+            res.winner = min(range(K), key=lambda r: (mism[r], r))
+            res.faulty = [r for r in range(K) if mism[r] > 0]
         per_area[area] = res
         total = [t + m for t, m in zip(total, res.mismatch)]
         unresolved += res.unresolved
         if first is None and res.first_div >= 0:
-            # replica 0 may hold the voted value when voting in place
+            # the in-place target (order[0], K >= 3) holds the voted value here
             after = getattr(h, "ready", None)
             raws = [backend.element_bytes(b, res.first_div, width, after=after) if after is not None
                     else backend.element_bytes(b, res.first_div, width) for b in bufs]
@@ -213,9 +231,10 @@ def vote_buffers_finish(backend, pending: list) -> VoteOutcome:
 
 
 def vote_buffers(backend, areas: Sequence[tuple], rel_tols: Sequence[float], ulp: Optional[int] = None,
-                 device: Optional[int] = None, in_place: bool = True) -> VoteOutcome:
+                 device: Optional[int] = None, in_place: bool = True,
+                 order: Optional[Sequence[int]] = None) -> VoteOutcome:
     """Synchronous K-way vote over device/host buffers (see vote_buffers_start)."""
-    return vote_buffers_finish(backend, vote_buffers_start(backend, areas, rel_tols, ulp, device, in_place))
+    return vote_buffers_finish(backend, vote_buffers_start(backend, areas, rel_tols, ulp, device, in_place, order))
 
 
 class DoneVote:

@@ -70,6 +70,11 @@ MATMUL_PARAMS = (Param.area("A", "r"), Param.area("B", "r"), Param.area("C", "w"
                  Param.scalar("n"))
 MATMUL_VARIANTS = (("mm_tc", "gpu-tc", mm_tc_body), ("mm_simt", "gpu-simt", mm_simt_body),
                    ("mm_tc3x", "gpu-tc3", mm_tc3x_body))
+# commit preference (Runtime.attach_kernel fidelity): the SIMT variant is
+# plain fp32 FFMA, the reference body's arithmetic (numpy fp32 sgemm);
+# 3xBF16 keeps ~fp32 operand precision; single-pass TF32 rounds operands to
+# 10 mantissa bits (~5e-5 relative).  A passing vote commits SIMT's buffer.
+MATMUL_FIDELITY = {"mm_simt": 0, "mm_tc3x": 1, "mm_tc": 2}
 
 
 # ---- reference 1-D tasks ---------------------------------------------------------------
@@ -149,6 +154,7 @@ class Workload:
                                                    Param.scalar("count")))
     input_fn: Callable = _uniform_input
     bind: Callable = _vector_bind
+    fidelity: dict = field(default_factory=dict)     # kernel -> attach_kernel fidelity rank
 
     def make_input(self, size: int, rng):
         return self.input_fn(size, rng)
@@ -157,7 +163,10 @@ class Workload:
         task = runtime.declare_task(self.name, self.params, float_delta=float_delta)
         for kernel, kind, body in self.variants:
             if kinds is None or kind in kinds:
-                runtime.attach_kernel(task, kernel, kind, body)
+                if self.fidelity:
+                    runtime.attach_kernel(task, kernel, kind, body, fidelity=self.fidelity.get(kernel, 0))
+                else:
+                    runtime.attach_kernel(task, kernel, kind, body)
         return task
 
 
@@ -202,7 +211,7 @@ _register(Workload("buggy-inc", "increment with a deterministic off-by-one bug i
                    oracle=_inc_oracle))
 _register(Workload("matmul", "C = A·B, fp32 n x n: tcgen05 TF32 / SIMT FP32 / tcgen05 3xBF16 variants",
                    list(MATMUL_VARIANTS), oracle=_matmul_oracle, params=MATMUL_PARAMS,
-                   input_fn=_matmul_input, bind=_matmul_bind))
+                   input_fn=_matmul_input, bind=_matmul_bind, fidelity=MATMUL_FIDELITY))
 
 
 def builtin_workloads() -> dict:

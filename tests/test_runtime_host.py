@@ -530,3 +530,63 @@ def test_overwrite_flag_reaches_the_bound_task():
                             "y": rt.register_data(bytes(16), 4, hf.ValueType.FLOAT32, "w"), "count": 4},
                         None, None)
     assert [p.overwrites for p in bound.params] == [False, True, False]
+
+
+# ---- commit preference (attach_kernel fidelity) ------------------------------------
+
+def _scaled_inc(scale):
+    def body(ctx):
+        n = ctx.arg("count")
+        src = ctx.request("input", "r")[:n]
+        ctx.request("output", "w")[:n] = (src + np.float32(1.0)) * np.float32(scale)
+    return body
+
+
+class TestCommitFidelity:
+    """A passing vote commits the agreeing replica of the best (lowest)
+    fidelity rank; K >= 3 votes prefer its values.  Default ranks keep the
+    reference's slot-0 commit (executor.py:268-274)."""
+
+    def _rt(self, fid, kinds=("cpu", "gpu")):
+        rt = hf.Runtime(hf.load_fleet(three_units()), hf.RuntimeConfig(), backend=HostBackend())
+        task = rt.declare_task("inc", IO)
+        # the variants agree within δ = 1e-3 but are bitwise distinct
+        scale = {"cpu": 1.0, "gpu": 1.0 + 2 ** -12}
+        for k in kinds:
+            rt.attach_kernel(task, f"inc_{k}", k, _scaled_inc(scale[k]), fidelity=fid.get(k, 0))
+        return rt, task
+
+    def test_default_ranks_commit_slot_zero(self):
+        rt, task = self._rt({})
+        _, o, a = args_for(rt)
+        rep = rt.invoke(task, a, DMR)
+        assert rep.votes == ["match"]
+        slot0 = rep.rounds_log[0]["slots"][0]
+        assert rep.committed.unit_id == slot0
+
+    @pytest.mark.parametrize("best", ["cpu", "gpu"], ids=["best-host", "best-accel"])
+    def test_dmr_commits_best_fidelity_replica_bitwise(self, best):
+        rt, task = self._rt({best: 0, ("gpu" if best == "cpu" else "cpu"): 5})
+        _, o, a = args_for(rt)
+        rep = rt.invoke(task, a, DMR)
+        assert rep.votes == ["match"] and rep.committed.kernel == f"inc_{best}"
+        scale = 1.0 if best == "cpu" else 1.0 + 2 ** -12
+        want = ((DATA + np.float32(1.0)) * np.float32(scale)).astype(np.float32)
+        assert rt.read_area(o) == want.tobytes()
+
+    def test_tmr_corrected_lands_in_best_replica_slot_order_counts(self):
+        cfg = three_units(gpu2={"corrupt_prob": 1.0, "corrupt_rel_magnitude": 0.5, "corrupt_element": 3})
+        rt = hf.Runtime(hf.load_fleet(cfg), hf.RuntimeConfig(), backend=HostBackend())
+        task = rt.declare_task("inc", IO)
+        rt.attach_kernel(task, "inc_cpu", "cpu", _scaled_inc(1.0), fidelity=1)
+        rt.attach_kernel(task, "inc_gpu", "gpu", _scaled_inc(1.0 + 2 ** -12), fidelity=0)
+        _, o, a = args_for(rt)
+        rep = rt.invoke(task, a, TMR)
+        assert rep.votes == ["corrected"]
+        log = rep.rounds_log[0]
+        # counts stay in slot order: only gpu2's slot mismatches
+        assert log["mismatch"][log["slots"].index("gpu2")] == 1 and sum(log["mismatch"]) == 1
+        assert rep.committed.unit_id == "gpu1"
+        got = np.frombuffer(rt.read_area(o), dtype=np.float32)
+        want = ((DATA + np.float32(1.0)) * np.float32(1.0 + 2 ** -12)).astype(np.float32)
+        assert got.tobytes() == want.tobytes()
