@@ -358,6 +358,11 @@ extern "C" int hf_gemm_simt(const float* A, const float* B, float* C, int M, int
         // HF_SGEMM_CHAIN=1 (A/B only): one fp32 chain over all of K, 48 KB
         const bool chain = hf::sgemm_chain();
         auto kern = chain ? hf::sgemm_128x128<0> : hf::sgemm_128x128<hf::SGEMM_CH>;
+        float* At = static_cast<float*>(hf::stream_scratch(device, st, 2, static_cast<size_t>(M) * K * sizeof(float)));
+        if (!At) {
+            hf::set_error("hf_gemm_simt: cannot allocate the A^T scratch");
+            return HF_ECUDA;
+        }
         // Co-scheduled: the A^T pre-pass runs on the device's greatest-priority
         // side stream, ahead of the tensor-core replica's pre-pass (level 1),
         // so this GEMM's grid is pending before the TC GEMM's and, launched on
