@@ -82,6 +82,10 @@ typedef struct hf_vote_result {
     int32_t verdict;            /* HF_VERDICT_*                              */
     int32_t K;
     int32_t reserved;
+    uint64_t first_raw0;        /* K >= 3: replica 0's raw element bits at
+                                   first_div as read, before an in-place vote
+                                   stored over it; 0 if none, K = 2 or
+                                   arbitrary widths                         */
 } hf_vote_result;
 
 /* ---- library -------------------------------------------------------- */
@@ -110,7 +114,7 @@ int hf_vote(const void* const* replicas, int K, int64_t n, int dtype,
 
 /* Asynchronous variant: writes the result to `dev_out` and returns without
  * synchronising.  `dev_out` may be device memory or pinned host memory
- * (device-visible through UVA): then the last CTA stores the 96-byte result
+ * (device-visible through UVA): then the last CTA stores the 104-byte result
  * straight over the bus and no separate read-back copy is needed.  `workspace` is caller-owned device memory
  * of hf_vote_workspace_bytes() bytes initialised once with
  * hf_vote_workspace_init(); the kernel leaves it re-initialised, so one

@@ -56,6 +56,7 @@ class HfVoteResult(ctypes.Structure):
         ("verdict", ctypes.c_int32),
         ("K", ctypes.c_int32),
         ("reserved", ctypes.c_int32),
+        ("first_raw0", ctypes.c_uint64),
     ]
 
 

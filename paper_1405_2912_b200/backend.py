@@ -147,7 +147,8 @@ class CudaBackend:
         dev = src_space.device
         cs = self.copy_stream(dev, "d2h")
         if after is not None:
-            cs.wait_event(after)
+            for ev in (after if isinstance(after, (list, tuple)) else [after]):
+                cs.wait_event(ev)
         else:
             cs.wait_stream(self.stream(dev))
         kernels.copy(dst_host, src, stream=cs)
@@ -402,6 +403,19 @@ class CudaBackend:
         stop = self.timer_stop(start, streams[lead], lead)
         return _PendingSliced(self, parts, K, stop)
 
+    def prewarm(self, devices, vote_slots: int = 4) -> None:
+        """Create each device's compute stream and a few vote result slots up
+        front.  A slot holds pinned host memory, and the first cudaHostAlloc of
+        a size waits for the device to go idle: made lazily inside a task's
+        vote it would wait out a hung replica before the executor's watchdog
+        gets to look at it."""
+        for d in sorted({d for d in devices if d is not None}):
+            self.stream(d)
+            slots = [self._vote_slot(d) for _ in range(vote_slots)]
+            for sl in slots:
+                self._release_vote_slot(d, sl)
+        torch.empty(8, dtype=torch.uint8, pin_memory=True)    # element_bytes' peek buffer size class
+
     def _vote_slot(self, device: int):
         with self._lock:
             pool = self._vote_slots.setdefault(device, [])
@@ -513,8 +527,8 @@ class _PendingSliced:
         for lo, d, slot in self._parts:
             r = _lib.HfVoteResult.from_buffer_copy(slot.host.numpy().tobytes())
             res.append(SliceResult(lo, [int(r.mismatch[i]) for i in range(self._K)], int(r.unresolved),
-                                   int(r.first_div)))
+                                   int(r.first_div), int(r.first_raw0)))
             self._be._release_vote_slot(d, slot)
         c = combine_slices(res, self._K)
         return kernels.VoteResult(c.verdict, c.mismatch, c.unresolved, c.first_div, c.winner, self._K,
-                                  c.faulty), ns
+                                  c.faulty, c.first_raw0), ns

@@ -935,8 +935,39 @@ static int launch(const void* A, const void* Bt, float* C, int M, int N, int K, 
                 HF_CUDA_CHECK(cudaMemsetAsync(sp.flags, 0, fbytes, st));
             }
         }
-        gemm_tf32_pair_kernel<PAIR_STAGES, BF16><<<2 * pairs, NUM_THREADS, pair_smem_bytes<PAIR_STAGES>(), st>>>(
-            ta, tb, C, M, N, K, sp);
+        // With the tail split, a fixup CTA spins on flags that partial CTAs
+        // of lower-numbered pairs publish (the split units of a tile are
+        // consecutive and the last, the fixup, has the highest pair), so the
+        // wait needs those CTAs co-resident.  A cooperative launch guarantees
+        // it (the grid is one persistent CTA per SM); if the device refuses
+        // one, the kernel runs without the split (whole tiles only, no
+        // inter-CTA waits) — same bytes per tile, just a ragged last round.
+        cudaError_t le = cudaSuccess;
+        if (sp.splits > 1) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(2 * pairs);
+            cfg.blockDim = dim3(NUM_THREADS);
+            cfg.dynamicSmemBytes = pair_smem_bytes<PAIR_STAGES>();
+            cfg.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeCooperative;
+            at[0].val.cooperative = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            le = cudaLaunchKernelEx(&cfg, gemm_tf32_pair_kernel<PAIR_STAGES, BF16>, ta, tb, C, M, N, K, sp);
+            static const bool verbose = getenv("HF_GEMM_TC_VERBOSE") != nullptr;
+            if (verbose)
+                fprintf(stderr, "hf_gemm_tc: pair kernel, %d tail tiles split %d ways, cooperative launch: %s\n",
+                        ptiles - sp.full_tiles, sp.splits, cudaGetErrorString(le));
+            if (le != cudaSuccess) {
+                cudaGetLastError();
+                cudaFreeAsync(sp.partial, st);
+                sp = PairSplit{ptiles, 1, nullptr, nullptr};
+            }
+        }
+        if (sp.splits == 1)
+            gemm_tf32_pair_kernel<PAIR_STAGES, BF16><<<2 * pairs, NUM_THREADS, pair_smem_bytes<PAIR_STAGES>(), st>>>(
+                ta, tb, C, M, N, K, sp);
         if (sp.partial) cudaFreeAsync(sp.partial, st);
         HF_CHECK_LAUNCH();
         return HF_OK;

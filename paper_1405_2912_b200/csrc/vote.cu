@@ -28,9 +28,14 @@
 #include <map>
 
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 namespace hf {
+
+// Upper bound on the vote grid (launch_vote clamps to it): per-block records
+// of the first divergence and replica 0's raw value there.
+constexpr int kMaxVoteBlocks = 2048;
 
 struct VoteWorkspace {
     unsigned long long mismatch[HF_MAX_K];
@@ -38,6 +43,12 @@ struct VoteWorkspace {
     unsigned long long first_div;  // min index; ~0ull = none
     unsigned int ticket;
     unsigned int pad;
+    // block b's lowest disagreeing element and replica 0's raw bits there
+    // (~0ull = none); the last block picks the global minimum's entry, so the
+    // reported value is replica 0's own even when the vote overwrote it in
+    // place, and re-arms the entries
+    unsigned long long blk_first[kMaxVoteBlocks];
+    unsigned long long blk_raw0[kMaxVoteBlocks];
 };
 
 constexpr int kMaxPairs = HF_MAX_K * (HF_MAX_K - 1) / 2;
@@ -184,12 +195,15 @@ __device__ __forceinline__ T extract(const uint4& v, int e) {
 }
 
 // Per-thread accumulators.
-template <int K>
+template <int K, typename RAW = unsigned long long>
 struct Acc {
     uint32_t mism[K];
     uint32_t unres;
     unsigned long long first;
+    RAW raw0;   // replica 0's bits at `first` (tracked for K >= 3, where votes run in place)
 };
+template <int DT, int K>
+using AccT = Acc<K, typename std::conditional<(sizeof(typename Elem<DT>::T) <= 4), uint32_t, unsigned long long>::type>;
 
 template <typename T, int K>
 struct Vals {
@@ -239,7 +253,7 @@ __device__ __noinline__ uint32_t vote_elem_slow(const Vals<typename Elem<DT>::T,
 // from its agreement mask.
 template <int DT, int K>
 __device__ __forceinline__ typename Elem<DT>::T vote_elem(const typename Elem<DT>::T (&x)[K],
-                                                           const VoteParams& p, Acc<K>& acc,
+                                                           const VoteParams& p, AccT<DT, K>& acc,
                                                            unsigned long long idx) {
     using E = Elem<DT>;
     if constexpr (DT == HF_F32) {
@@ -285,7 +299,10 @@ __device__ __forceinline__ typename Elem<DT>::T vote_elem(const typename Elem<DT
     }
 #pragma unroll
     for (int r = 0; r < K; ++r) acc.mism[r] += (dis >> r) & 1u;
-    if (acc.first == ~0ull) acc.first = idx;
+    if (acc.first == ~0ull) {
+        acc.first = idx;
+        if constexpr (K >= 3) acc.raw0 = static_cast<decltype(acc.raw0)>(x[0]);
+    }
     typename E::T out = x[0];
 #pragma unroll
     for (int r = 1; r < K; ++r)
@@ -299,11 +316,12 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
     using T = typename E::T;
     constexpr int PV = E::kPerVec;
 
-    Acc<K> acc;
+    AccT<DT, K> acc;
 #pragma unroll
     for (int r = 0; r < K; ++r) acc.mism[r] = 0;
     acc.unres = 0;
     acc.first = ~0ull;
+    acc.raw0 = 0;
 
     const long long gtid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     const long long gstride = static_cast<long long>(gridDim.x) * blockDim.x;
@@ -403,7 +421,7 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
 
     // ---- reduction: warp -> block (smem) -> one atomic per block ----------
     __shared__ unsigned long long s_cnt[K + 1];
-    __shared__ unsigned long long s_first;
+    __shared__ unsigned long long s_first, s_raw0;
     __shared__ bool s_last;
     if (threadIdx.x <= K) s_cnt[threadIdx.x] = 0;
     if (threadIdx.x == 0) s_first = ~0ull;
@@ -428,6 +446,9 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
         if (lane == 0) atomicMin(&s_first, f);
     }
     __syncthreads();
+    // element indices are unique per thread: one thread holds the block minimum
+    if (K >= 3 && s_first != ~0ull && acc.first == s_first) s_raw0 = acc.raw0;
+    __syncthreads();
     if (threadIdx.x == 0) {
         VoteWorkspace* ws = p.ws;
 #pragma unroll
@@ -435,13 +456,31 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
             unsigned long long c = s_cnt[r];
             if (c) atomicAdd(r < K ? &ws->mismatch[r] : &ws->unresolved, c);
         }
-        if (s_first != ~0ull) atomicMin(&ws->first_div, s_first);
+        if (s_first != ~0ull) {
+            atomicMin(&ws->first_div, s_first);
+            if (K >= 3) {
+                ws->blk_first[blockIdx.x] = s_first;
+                ws->blk_raw0[blockIdx.x] = s_raw0;
+            }
+        }
         __threadfence();
         unsigned int t = atomicAdd(&ws->ticket, 1u);
         s_last = (t == gridDim.x - 1);
     }
     __syncthreads();
     // ---- last block: finalise the result and re-arm the workspace ----------
+    if (K >= 3 && s_last) {
+        __threadfence();
+        const unsigned long long fd = *(volatile unsigned long long*)&p.ws->first_div;
+        if (fd != ~0ull) {       // whose record is the global minimum (then re-arm them all)
+            volatile unsigned long long* bf = p.ws->blk_first;
+            for (unsigned int b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+                if (bf[b] == fd) s_raw0 = p.ws->blk_raw0[b];
+                bf[b] = ~0ull;
+            }
+        }
+        __syncthreads();
+    }
     if (s_last && threadIdx.x == 0) {
         __threadfence();
         VoteWorkspace* ws = p.ws;
@@ -469,6 +508,7 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
         out->verdict = unres > 0 ? HF_VERDICT_MISMATCH : (any ? HF_VERDICT_CORRECTED : HF_VERDICT_MATCH);
         out->K = K;
         out->reserved = 0;
+        out->first_raw0 = (K < 3 || fd == ~0ull) ? 0ull : s_raw0;
         for (int r = 0; r < HF_MAX_K; ++r) ws->mismatch[r] = 0;
         ws->unresolved = 0;
         ws->first_div = ~0ull;
@@ -576,6 +616,7 @@ __global__ void __launch_bounds__(256) vote_bytes_kernel(const __grid_constant__
         out->verdict = unres > 0 ? HF_VERDICT_MISMATCH : (any ? HF_VERDICT_CORRECTED : HF_VERDICT_MATCH);
         out->K = K;
         out->reserved = 0;
+        out->first_raw0 = 0;     // arbitrary widths: replica bytes are read back by the host
         for (int r = 0; r < HF_MAX_K; ++r) ws->mismatch[r] = 0;
         ws->unresolved = 0;
         ws->first_div = ~0ull;
@@ -585,6 +626,11 @@ __global__ void __launch_bounds__(256) vote_bytes_kernel(const __grid_constant__
 }
 
 __global__ void ws_init_kernel(VoteWorkspace* ws) {
+    for (int b = threadIdx.x; b < kMaxVoteBlocks; b += blockDim.x) {
+        ws->blk_first[b] = ~0ull;
+        ws->blk_raw0[b] = 0;
+    }
+    if (threadIdx.x != 0) return;
     for (int r = 0; r < HF_MAX_K; ++r) ws->mismatch[r] = 0;
     ws->unresolved = 0;
     ws->first_div = ~0ull;
@@ -729,6 +775,7 @@ static int launch_vote(VoteParams& p, int K, int dtype, int width, int device, c
         // second wave of a memory-bound grid
         static const int legacy = getenv("HF_VOTE_GRID_LEGACY") != nullptr;   // A/B timing only
         long long cap = static_cast<long long>(sms) * (legacy ? 8 : resident_ctas(reinterpret_cast<const void*>(k), device));
+        if (cap > kMaxVoteBlocks) cap = kMaxVoteBlocks;
         int grid = static_cast<int>(want < cap ? want : cap);
         // programmatic dependent launch (HF_PDL=0 disables, A/B only):
         // back-to-back 64 MiB K=2 votes 23.5 -> 21.7 us (tools/vote_ab.py)
@@ -772,7 +819,7 @@ static int acquire_slot(int device, SyncSlot& out) {
     HF_CUDA_CHECK(cudaMalloc(&s.ws, sizeof(VoteWorkspace)));
     HF_CUDA_CHECK(cudaMalloc(&s.dres, sizeof(hf_vote_result)));
     HF_CUDA_CHECK(cudaMallocHost(&s.hres, sizeof(hf_vote_result)));
-    ws_init_kernel<<<1, 1>>>(s.ws);
+    ws_init_kernel<<<1, 256>>>(s.ws);
     HF_CHECK_LAUNCH();
     HF_CUDA_CHECK(cudaDeviceSynchronize());
     out = s;
@@ -854,7 +901,7 @@ int hf_vote_workspace_init(void* workspace, int device, void* stream) {
     HF_REQUIRE(workspace != nullptr, "hf_vote_workspace_init: NULL workspace");
     hf::DeviceGuard g(device);
     HF_REQUIRE(g.ok, "hf_vote_workspace_init: cannot select device %d", device);
-    hf::ws_init_kernel<<<1, 1, 0, hf::as_stream(stream)>>>(static_cast<hf::VoteWorkspace*>(workspace));
+    hf::ws_init_kernel<<<1, 256, 0, hf::as_stream(stream)>>>(static_cast<hf::VoteWorkspace*>(workspace));
     HF_CHECK_LAUNCH();
     return HF_OK;
 }

@@ -47,7 +47,7 @@ def pathfinder_fleet_config() -> dict:
 
 def b200_fleet_config() -> dict:
     """One B200, three diverse matmul units (tcgen05 TF32, SIMT FP32,
-    tcgen05 3xTF32) sharing its HBM, plus an HBM checkpoint space."""
+    tcgen05 3xBF16) sharing its HBM, plus an HBM checkpoint space."""
     cfg = gpu_fleet_config(devices=(0,), kinds=("gpu-tc", "gpu-simt", "gpu-tc3"))
     cfg["memory_spaces"].append({"id": "gpu0ckpt", "label": "HBM checkpoint reserve", "device": 0})
     return cfg

@@ -69,13 +69,16 @@ class VoteResult:
     winner: int
     K: int
     faulty: list[int] = field(default_factory=list)
+    first_raw0: Optional[int] = None  # replica 0's raw bits at first_div, as read before an in-place store
 
     @classmethod
     def from_c(cls, r: HfVoteResult) -> "VoteResult":
         K = int(r.K)
         mism = [int(r.mismatch[i]) for i in range(K)]
-        return cls(_lib.VERDICT_NAMES[int(r.verdict)], mism, int(r.unresolved), int(r.first_div),
-                   int(r.winner), K, [i for i, m in enumerate(mism) if m > 0])
+        fd = int(r.first_div)
+        return cls(_lib.VERDICT_NAMES[int(r.verdict)], mism, int(r.unresolved), fd,
+                   int(r.winner), K, [i for i, m in enumerate(mism) if m > 0],
+                   int(r.first_raw0) if fd >= 0 else None)
 
 
 def _ptr_array(ts: Sequence[torch.Tensor]):
@@ -178,7 +181,7 @@ def vote_async(replicas: Sequence[torch.Tensor], ws: VoteWorkspace, rel_tol=0.00
                voted: Optional[torch.Tensor] = None,
                stream: Optional[torch.cuda.Stream] = None,
                result_into: Optional[torch.Tensor] = None) -> None:
-    """result_into: a pinned host buffer of sizeof(HfVoteResult) bytes that
+    """result_into: a pinned host buffer of sizeof(HfVoteResult) (104) bytes that
     receives the result directly (default: ws.result in device memory)."""
     K = len(replicas)
     n = replicas[0].numel()
@@ -244,12 +247,13 @@ def vote_sliced(replicas: Sequence[torch.Tensor], rel_tol=0.001, ulp_tol=None,
     for lo, slot, ev in pending:
         ev.synchronize()
         r = HfVoteResult.from_buffer_copy(slot.host.numpy().tobytes())
-        parts.append(SliceResult(lo, [int(r.mismatch[i]) for i in range(K)], int(r.unresolved), int(r.first_div)))
+        parts.append(SliceResult(lo, [int(r.mismatch[i]) for i in range(K)], int(r.unresolved), int(r.first_div),
+                                 int(r.first_raw0)))
     c = combine_slices(parts, K)
     verdict_code = {"match": _lib.HF_VERDICT_MATCH, "corrected": _lib.HF_VERDICT_CORRECTED,
                     "mismatch": _lib.HF_VERDICT_MISMATCH}[c.verdict]
     return VoteResult(_lib.VERDICT_NAMES[verdict_code], c.mismatch, c.unresolved, c.first_div, c.winner, K,
-                      c.faulty)
+                      c.faulty, c.first_raw0)
 
 
 # ---- copy / checkpoint ------------------------------------------------------

@@ -59,6 +59,7 @@ class SliceResult:
     mismatch: list
     unresolved: int
     first_div: int          # -1 when the slice agrees everywhere
+    first_raw0: Optional[int] = None   # replica 0's raw bits at first_div
 
 
 @dataclass
@@ -68,6 +69,7 @@ class CombinedVote:
     unresolved: int
     first_div: int
     winner: int
+    first_raw0: Optional[int] = None
 
     @property
     def faulty(self) -> list:
@@ -80,16 +82,18 @@ def combine_slices(parts: Sequence[SliceResult], k: int) -> CombinedVote:
     mism = [0] * k
     unres = 0
     first: Optional[int] = None
+    raw0 = None
     for p in parts:
         for r in range(k):
             mism[r] += int(p.mismatch[r])
         unres += int(p.unresolved)
         if p.first_div >= 0:
             g = p.lo + int(p.first_div)
-            first = g if first is None else min(first, g)
+            if first is None or g < first:
+                first, raw0 = g, p.first_raw0
     winner = min(range(k), key=lambda r: (mism[r], r))
     verdict = "mismatch" if unres else ("corrected" if any(mism) else "match")
-    return CombinedVote(verdict, mism, unres, -1 if first is None else first, winner)
+    return CombinedVote(verdict, mism, unres, -1 if first is None else first, winner, raw0)
 
 
 def max_over_ranks(value: float, device=None) -> float:

@@ -214,10 +214,18 @@ def vote_buffers_finish(backend, pending: list) -> VoteOutcome:
         total = [t + m for t, m in zip(total, res.mismatch)]
         unresolved += res.unresolved
         if first is None and res.first_div >= 0:
-            # the in-place target (order[0], K >= 3) holds the voted value here
+            # the in-place target (order[0], K >= 3) holds the voted value at
+            # first_div by now; the kernel reports its own value as it read it
             after = getattr(h, "ready", None)
-            raws = [backend.element_bytes(b, res.first_div, width, after=after) if after is not None
-                    else backend.element_bytes(b, res.first_div, width) for b in bufs]
+            own0 = getattr(res, "first_raw0", None) if K >= 3 and width <= 8 else None
+            raws = []
+            for r, b in enumerate(bufs):
+                if r == order[0] and own0 is not None:
+                    raws.append(int(own0).to_bytes(8, "little")[:width])
+                elif after is not None:
+                    raws.append(backend.element_bytes(b, res.first_div, width, after=after))
+                else:
+                    raws.append(backend.element_bytes(b, res.first_div, width))
             vals = [_element(r, vt, width, 0) for r in raws]
             first = (area, res.first_div, vals[0], vals[1]) if K == 2 else (area, res.first_div, tuple(vals))
     if unresolved:

@@ -98,6 +98,16 @@ def test_tmr_simt_fault_takes_next_best_value(operands):
     want = simt.reshape(-1).copy()
     want[elem] = tc3.reshape(-1)[elem]      # 3xBF16 ranks next: its value fills the faulty element
     assert out.reshape(-1).tobytes() == want.tobytes()
+    # the reported divergence values are each replica's own: the SIMT entry
+    # is the flipped value the kernel read, not the voted value it stored
+    # over it in place (hf_vote_result.first_raw0)
+    log = rep.rounds_log[0]
+    area, idx, vals = log["first_divergence"] if len(log["first_divergence"]) == 3 else (None, None, None)
+    assert idx == elem
+    flipped = simt.reshape(-1)[elem:elem + 1].copy()
+    flipped.view(np.uint32)[0] ^= np.uint32(1 << 30)
+    assert vals[log["slots"].index("gpu0.simt")] == float(flipped[0])
+    assert vals[log["slots"].index("gpu0.tc3")] == float(tc3.reshape(-1)[elem])
 
 
 def test_committed_error_vs_binary64(operands):

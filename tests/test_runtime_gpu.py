@@ -390,3 +390,75 @@ def test_reserve_presizes_the_device_heap():
     del bufs
     with pytest.raises(hf.UnknownSpaceError):
         rt.reserve("nowhere", nb, 1)
+
+
+def _hang_runtime(devices, deadline_ns=50_000_000):
+    spaces = [{"id": "host", "host": True}] + [{"id": f"g{d}mem", "device": d} for d in devices]
+    units = []
+    for d in devices:
+        # two units per kind: after the hung unit's timeout quarantines it
+        # (reference rating rule), HetDMR still finds a diverse pair
+        units += [{"id": f"g{d}.{k}{i}", "kind": f"gpu-{k}", "memory_space": f"g{d}mem", "timing": "measured"}
+                  for k in "ab" for i in (1, 2)]
+    rt = hf.Runtime(hf.load_fleet({"memory_spaces": spaces, "units": units}),
+                    hf.RuntimeConfig(default_deadline_ns=deadline_ns, attempt_limit=20))
+    task = rt.declare_task("copy", COPY_PARAMS)
+    calls = []
+
+    def body(ctx):
+        if not calls:
+            kernels.debug_spin(1_500_000_000, stream=ctx.stream, device=ctx.device)   # a 1.5 s hang
+        calls.append(ctx.device)
+        _copy_body(ctx)
+
+    rt.attach_kernel(task, "ka", "gpu-a", body)
+    rt.attach_kernel(task, "kb", "gpu-b", body)
+    return rt, task
+
+
+def test_task_stream_hang_is_bounded_on_one_gpu():
+    """TaskStream (deferred timing, vote launched before the replicas are
+    known to finish): a hung replica must not block the host.  Its vote
+    already joined GPU 0's compute stream to the hung stream, so GPU 0 is
+    wedged; with no other device the re-dispatch has no candidate and the
+    task fails fast with the mapper's error instead of waiting out the hang.
+    Once the spin drains, the device returns to service."""
+    import time as _time
+    rt, task = _hang_runtime([0])
+    n = 1 << 20
+    data = np.random.default_rng(2).uniform(1, 2, n).astype(np.float32)
+    inp = rt.register_data(data.tobytes(), n, hf.ValueType.FLOAT32, "r")
+    out = rt.register_data(bytes(4 * n), n, hf.ValueType.FLOAT32, "w")
+    torch.cuda.synchronize()
+    t0 = _time.perf_counter()
+    with pytest.raises((hf.StrategyInfeasibleError, hf.UnrecoverableTaskError)):
+        with rt.task_stream(depth=1) as ts:
+            ts.submit(task, {"input": inp, "output": out, "count": n}, hf.Strategy(hf.StrategyKind.HET_DMR))
+    assert _time.perf_counter() - t0 < 1.0, "the host waited out the hang"
+    assert rt.executor._wedged and any(not k.endswith("#stranded") for k in rt.executor._hung)
+    torch.cuda.synchronize()          # the spin ends (<= 1.5 s)
+    rt.executor._reap_hung()
+    assert not rt.executor._wedged
+    out2 = rt.register_data(bytes(4 * n), n, hf.ValueType.FLOAT32, "w")
+    with rt.task_stream(depth=1) as ts:
+        rep = ts.submit(task, {"input": inp, "output": out2, "count": n}, hf.Strategy(hf.StrategyKind.HET_DMR))
+    assert rep.success and rep.votes == ["match"]
+    assert np.array_equal(rt.read_array(out2), data)
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_task_stream_hang_redispatches_to_another_gpu():
+    import time as _time
+    rt, task = _hang_runtime([0, 1])
+    n = 1 << 20
+    data = np.random.default_rng(3).uniform(1, 2, n).astype(np.float32)
+    inp = rt.register_data(data.tobytes(), n, hf.ValueType.FLOAT32, "r")
+    out = rt.register_data(bytes(4 * n), n, hf.ValueType.FLOAT32, "w")
+    torch.cuda.synchronize()
+    t0 = _time.perf_counter()
+    with rt.task_stream(depth=1) as ts:
+        rep = ts.submit(task, {"input": inp, "output": out, "count": n}, hf.Strategy(hf.StrategyKind.HET_DMR))
+    assert _time.perf_counter() - t0 < 1.0
+    assert rep.success and rep.fault_counts["timeout"] == 1
+    assert np.array_equal(rt.read_array(out), data)
+    assert rep.committed.unit_id.startswith("g1.")

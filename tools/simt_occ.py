@@ -1,6 +1,6 @@
 """SIMT GEMM at one vs two CTAs per SM (HF_SGEMM_COSCHED_SMEM in the
 environment sets the co-scheduling smem reservation), alone and with the TC
-and 3xTF32 replicas on concurrent streams (the HetTMR round on one GPU)."""
+and 3xBF16 replicas on concurrent streams (the HetTMR round on one GPU)."""
 import json, os, sys, statistics
 from pathlib import Path
 import torch
