@@ -86,6 +86,10 @@ typedef struct hf_vote_result {
                                    first_div as read, before an in-place vote
                                    stored over it; 0 if none, K = 2 or
                                    arbitrary widths                         */
+    int64_t  kernel_ns;         /* the vote kernel's own device time: earliest
+                                   CTA start (after its stream dependency) to
+                                   the last CTA's finalisation, %globaltimer;
+                                   0 for arbitrary widths                   */
 } hf_vote_result;
 
 /* ---- library -------------------------------------------------------- */
@@ -114,7 +118,7 @@ int hf_vote(const void* const* replicas, int K, int64_t n, int dtype,
 
 /* Asynchronous variant: writes the result to `dev_out` and returns without
  * synchronising.  `dev_out` may be device memory or pinned host memory
- * (device-visible through UVA): then the last CTA stores the 104-byte result
+ * (device-visible through UVA): then the last CTA stores the 112-byte result
  * straight over the bus and no separate read-back copy is needed.  `workspace` is caller-owned device memory
  * of hf_vote_workspace_bytes() bytes initialised once with
  * hf_vote_workspace_init(); the kernel leaves it re-initialised, so one

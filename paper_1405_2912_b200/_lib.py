@@ -57,6 +57,7 @@ class HfVoteResult(ctypes.Structure):
         ("K", ctypes.c_int32),
         ("reserved", ctypes.c_int32),
         ("first_raw0", ctypes.c_uint64),
+        ("kernel_ns", ctypes.c_int64),
     ]
 
 

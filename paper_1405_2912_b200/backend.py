@@ -455,7 +455,8 @@ class CudaBackend:
                 streams[devs[0]].wait_stream(streams[d])
             stop = self.timer_stop(start, streams[devs[0]], devs[0])
             self.launches += len(devs)
-            return res, stop()
+            ns = stop()
+            return res, (res.kernel_ns or ns)
         st = self.stream(device)
         for d in devs:
             if d != device:
@@ -470,7 +471,8 @@ class CudaBackend:
                                device=device, stream=st)
         stop = self.timer_stop(start, st, device)
         self.launches += 1
-        return res, stop()
+        ns = stop()
+        return res, (getattr(res, "kernel_ns", 0) or ns)
 
 
 class _NullScope:
@@ -510,7 +512,10 @@ class _PendingVote:
         ns = self._stop()            # synchronises the stop event (after the vote kernel)
         raw = self._slot.host.numpy().tobytes()
         self._be._release_vote_slot(self._dev, self._slot)
-        return kernels.VoteResult.from_c(_lib.HfVoteResult.from_buffer_copy(raw)), ns
+        res = kernels.VoteResult.from_c(_lib.HfVoteResult.from_buffer_copy(raw))
+        # the kernel's own clock: the event pair around the launch also counts
+        # any GPU idle time while the host was still issuing the vote
+        return res, (res.kernel_ns or ns)
 
 
 class _PendingSliced:
@@ -524,11 +529,13 @@ class _PendingSliced:
         from .sharding import SliceResult, combine_slices
         ns = self._stop()             # the lead stream waited for every slice's stream
         res = []
+        kns = 0
         for lo, d, slot in self._parts:
             r = _lib.HfVoteResult.from_buffer_copy(slot.host.numpy().tobytes())
+            kns = max(kns, int(r.kernel_ns))
             res.append(SliceResult(lo, [int(r.mismatch[i]) for i in range(self._K)], int(r.unresolved),
                                    int(r.first_div), int(r.first_raw0)))
             self._be._release_vote_slot(d, slot)
         c = combine_slices(res, self._K)
         return kernels.VoteResult(c.verdict, c.mismatch, c.unresolved, c.first_div, c.winner, self._K,
-                                  c.faulty, c.first_raw0), ns
+                                  c.faulty, c.first_raw0, kns), (kns or ns)

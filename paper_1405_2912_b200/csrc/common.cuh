@@ -137,6 +137,13 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 // ---- device utilities ----------------------------------------------------
 namespace hf {
 
+// Global nanosecond timer (same clock on every SM).
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 // PDL: wait for the previous grid of the stream (no-op without PDL launch).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 // PDL: let the stream's next grid start launching.

@@ -43,6 +43,7 @@ struct VoteWorkspace {
     unsigned long long first_div;  // min index; ~0ull = none
     unsigned int ticket;
     unsigned int pad;
+    unsigned long long t_start;    // earliest CTA start (%globaltimer ns); ~0ull = armed
     // block b's lowest disagreeing element and replica 0's raw bits there
     // (~0ull = none); the last block picks the global minimum's entry, so the
     // reported value is replica 0's own even when the vote overwrote it in
@@ -331,6 +332,9 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
     // rasterisation overlap that kernel's tail); nothing is read before the
     // previous grid has completed and flushed.
     pdl_wait();
+    // the kernel's own device time (result.kernel_ns): earliest CTA start
+    // after the dependency wait .. the last CTA's finalisation
+    if (threadIdx.x == 0) atomicMin(&p.ws->t_start, globaltimer_ns());
 
     // ---- vector loop: UNROLL x K 128-bit loads in flight per thread ----
     long long j = gtid;
@@ -509,9 +513,11 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
         out->K = K;
         out->reserved = 0;
         out->first_raw0 = (K < 3 || fd == ~0ull) ? 0ull : s_raw0;
+        out->kernel_ns = static_cast<long long>(globaltimer_ns() - *(volatile unsigned long long*)&ws->t_start);
         for (int r = 0; r < HF_MAX_K; ++r) ws->mismatch[r] = 0;
         ws->unresolved = 0;
         ws->first_div = ~0ull;
+        ws->t_start = ~0ull;
         __threadfence();
         ws->ticket = 0;
     }
@@ -617,6 +623,7 @@ __global__ void __launch_bounds__(256) vote_bytes_kernel(const __grid_constant__
         out->K = K;
         out->reserved = 0;
         out->first_raw0 = 0;     // arbitrary widths: replica bytes are read back by the host
+        out->kernel_ns = 0;
         for (int r = 0; r < HF_MAX_K; ++r) ws->mismatch[r] = 0;
         ws->unresolved = 0;
         ws->first_div = ~0ull;
@@ -636,6 +643,7 @@ __global__ void ws_init_kernel(VoteWorkspace* ws) {
     ws->first_div = ~0ull;
     ws->ticket = 0;
     ws->pad = 0;
+    ws->t_start = ~0ull;
 }
 
 #define HF_VOTE_K(DT) (const void*)vote_kernel<DT, 2, 2>, (const void*)vote_kernel<DT, 3, 2>, \

@@ -70,6 +70,7 @@ class VoteResult:
     K: int
     faulty: list[int] = field(default_factory=list)
     first_raw0: Optional[int] = None  # replica 0's raw bits at first_div, as read before an in-place store
+    kernel_ns: int = 0                # the vote kernel's own device time (max over slices when sliced)
 
     @classmethod
     def from_c(cls, r: HfVoteResult) -> "VoteResult":
@@ -78,7 +79,7 @@ class VoteResult:
         fd = int(r.first_div)
         return cls(_lib.VERDICT_NAMES[int(r.verdict)], mism, int(r.unresolved), fd,
                    int(r.winner), K, [i for i, m in enumerate(mism) if m > 0],
-                   int(r.first_raw0) if fd >= 0 else None)
+                   int(r.first_raw0) if fd >= 0 else None, int(r.kernel_ns))
 
 
 def _ptr_array(ts: Sequence[torch.Tensor]):
@@ -244,16 +245,18 @@ def vote_sliced(replicas: Sequence[torch.Tensor], rel_tol=0.001, ulp_tol=None,
         ev.record(st)
         pending.append((lo, slot, ev))
     parts = []
+    kns = 0
     for lo, slot, ev in pending:
         ev.synchronize()
         r = HfVoteResult.from_buffer_copy(slot.host.numpy().tobytes())
         parts.append(SliceResult(lo, [int(r.mismatch[i]) for i in range(K)], int(r.unresolved), int(r.first_div),
                                  int(r.first_raw0)))
+        kns = max(kns, int(r.kernel_ns))
     c = combine_slices(parts, K)
     verdict_code = {"match": _lib.HF_VERDICT_MATCH, "corrected": _lib.HF_VERDICT_CORRECTED,
                     "mismatch": _lib.HF_VERDICT_MISMATCH}[c.verdict]
     return VoteResult(_lib.VERDICT_NAMES[verdict_code], c.mismatch, c.unresolved, c.first_div, c.winner, K,
-                      c.faulty, c.first_raw0)
+                      c.faulty, c.first_raw0, kns)
 
 
 # ---- copy / checkpoint ------------------------------------------------------

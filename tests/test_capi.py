@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_result_struct_layout_matches_header():
     from paper_1405_2912_b200._lib import HfVoteResult
-    assert ctypes.sizeof(HfVoteResult) == 8 * 8 + 8 + 8 + 4 * 4 + 8
+    assert ctypes.sizeof(HfVoteResult) == 8 * 8 + 8 + 8 + 4 * 4 + 8 + 8
 
 
 def test_no_device_reports_cleanly():
