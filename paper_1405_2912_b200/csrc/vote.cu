@@ -334,7 +334,9 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
     pdl_wait();
     // the kernel's own device time (result.kernel_ns): earliest CTA start
     // after the dependency wait .. the last CTA's finalisation
-    if (threadIdx.x == 0) atomicMin(&p.ws->t_start, globaltimer_ns());
+    // (block 0 is dispatched first; its thread 0 stores the reading with the
+    // block's counts at the end, so the timer latency overlaps its loads)
+    const unsigned long long t_begin = (blockIdx.x == 0 && threadIdx.x == 0) ? globaltimer_ns() : 0ull;
 
     // ---- vector loop: UNROLL x K 128-bit loads in flight per thread ----
     long long j = gtid;
@@ -344,7 +346,7 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
         for (int u = 0; u < UNROLL; ++u)
 #pragma unroll
             for (int r = 0; r < K; ++r)
-                v[u][r] = (r == 0 && p.in_place)
+                v[u][r] = (K >= 3 && r == 0 && p.in_place)
                               ? ld_stream_rw(reinterpret_cast<const uint4*>(p.rep[r]) + (j + u * gstride))
                               : ld_stream(reinterpret_cast<const uint4*>(p.rep[r]) + (j + u * gstride));
 #pragma unroll
@@ -391,8 +393,8 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
         uint4 v[K];
 #pragma unroll
         for (int r = 0; r < K; ++r)
-            v[r] = (r == 0 && p.in_place) ? ld_stream_rw(reinterpret_cast<const uint4*>(p.rep[r]) + j)
-                                          : ld_stream(reinterpret_cast<const uint4*>(p.rep[r]) + j);
+            v[r] = (K >= 3 && r == 0 && p.in_place) ? ld_stream_rw(reinterpret_cast<const uint4*>(p.rep[r]) + j)
+                                                    : ld_stream(reinterpret_cast<const uint4*>(p.rep[r]) + j);
         T o[PV];
         bool changed = false;
 #pragma unroll
@@ -414,8 +416,8 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
         T x[K];
 #pragma unroll
         for (int r = 0; r < K; ++r)
-            x[r] = (r == 0 && p.in_place) ? reinterpret_cast<const volatile T*>(p.rep[r])[i]
-                                          : __ldg(reinterpret_cast<const T*>(p.rep[r]) + i);
+            x[r] = (K >= 3 && r == 0 && p.in_place) ? reinterpret_cast<const volatile T*>(p.rep[r])[i]
+                                                    : __ldg(reinterpret_cast<const T*>(p.rep[r]) + i);
         T o = vote_elem<DT, K>(x, p, acc, static_cast<unsigned long long>(i));
         if (p.voted != nullptr && (!p.in_place || o != x[0])) reinterpret_cast<T*>(p.voted)[i] = o;
     }
@@ -449,11 +451,14 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
         }
         if (lane == 0) atomicMin(&s_first, f);
     }
+    __shared__ unsigned long long s_fd, s_t0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) s_t0 = t_begin;   // for whichever thread leads the epilogue
     __syncthreads();
-    // element indices are unique per thread: one thread holds the block minimum
-    if (K >= 3 && s_first != ~0ull && acc.first == s_first) s_raw0 = acc.raw0;
-    __syncthreads();
-    if (threadIdx.x == 0) {
+    // the block's epilogue thread: for K >= 3 the one holding the block's
+    // first divergence (element indices are unique per thread) so it can
+    // publish replica 0's value there without another barrier, else thread 0
+    const bool leader = (K >= 3 && s_first != ~0ull) ? acc.first == s_first : threadIdx.x == 0;
+    if (leader) {
         VoteWorkspace* ws = p.ws;
 #pragma unroll
         for (int r = 0; r <= K; ++r) {
@@ -464,29 +469,31 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
             atomicMin(&ws->first_div, s_first);
             if (K >= 3) {
                 ws->blk_first[blockIdx.x] = s_first;
-                ws->blk_raw0[blockIdx.x] = s_raw0;
+                ws->blk_raw0[blockIdx.x] = static_cast<unsigned long long>(acc.raw0);
             }
         }
+        if (blockIdx.x == 0) ws->t_start = s_t0;
         __threadfence();
         unsigned int t = atomicAdd(&ws->ticket, 1u);
         s_last = (t == gridDim.x - 1);
+        if (s_last) {
+            __threadfence();
+            s_fd = *(volatile unsigned long long*)&ws->first_div;
+        }
     }
     __syncthreads();
     // ---- last block: finalise the result and re-arm the workspace ----------
-    if (K >= 3 && s_last) {
-        __threadfence();
-        const unsigned long long fd = *(volatile unsigned long long*)&p.ws->first_div;
-        if (fd != ~0ull) {       // whose record is the global minimum (then re-arm them all)
-            volatile unsigned long long* bf = p.ws->blk_first;
-            for (unsigned int b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
-                if (bf[b] == fd) s_raw0 = p.ws->blk_raw0[b];
-                bf[b] = ~0ull;
-            }
+    if (K >= 3 && s_last && s_fd != ~0ull) {
+        // whose record is the global minimum (then re-arm them all)
+        volatile unsigned long long* bf = p.ws->blk_first;
+        for (unsigned int b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+            if (bf[b] == s_fd) s_raw0 = p.ws->blk_raw0[b];
+            bf[b] = ~0ull;
         }
         __syncthreads();
     }
     if (s_last && threadIdx.x == 0) {
-        __threadfence();
+        const unsigned long long t_end = globaltimer_ns();   // latency overlaps the reads below
         VoteWorkspace* ws = p.ws;
         hf_vote_result* out = p.out;
         volatile unsigned long long* vm = ws->mismatch;
@@ -513,7 +520,7 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
         out->K = K;
         out->reserved = 0;
         out->first_raw0 = (K < 3 || fd == ~0ull) ? 0ull : s_raw0;
-        out->kernel_ns = static_cast<long long>(globaltimer_ns() - *(volatile unsigned long long*)&ws->t_start);
+        out->kernel_ns = static_cast<long long>(t_end - *(volatile unsigned long long*)&ws->t_start);
         for (int r = 0; r < HF_MAX_K; ++r) ws->mismatch[r] = 0;
         ws->unresolved = 0;
         ws->first_div = ~0ull;
