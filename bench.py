@@ -584,7 +584,7 @@ def run_hetft_arm(args, rank, world, local):
     simt_tflops = flops / (simt_ms * 1e-3) / 1e12 if simt_ms else None
     sm_max = (clocks or {}).get("sm_max_mhz") or 1965.0
     ffma_peak, ffma_src = fp32_peak(sm_max)
-    traffic = ncu_traffic("sgemm_128x128", "transpose_a")
+    traffic = ncu_traffic("sgemm_128x128<32>", "transpose_a")
     vote_gbs = (3 * nb * sum(stats["votes"].values())) / (stats["vote_ns"] * 1e-9) / 1e9 if stats["vote_ns"] else None
     cpu = None
     if not args.no_cpu_baseline:

@@ -1,4 +1,6 @@
-"""Minimal driver for ncu captures: each hot kernel at the bench size, 3x."""
+"""Minimal driver for ncu captures: each hot kernel once at the bench size,
+in the launch shapes a one-GPU HetTMR task uses (co-scheduling flag) and the
+standalone shapes of the roofline measurements."""
 import sys
 from pathlib import Path
 
@@ -8,6 +10,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_1405_2912_b200 import kernels  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
+reps_ = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 d = "cuda:0"
 m = n * n
 base = torch.rand(m, device=d) + 1
@@ -16,11 +19,12 @@ kernels.inject_bitflip(reps[2], m // 3, 27)
 a, b = base.view(n, n), reps[1].view(n, n)
 c = torch.empty(n, n, device=d)
 dst = torch.empty_like(base)
-for _ in range(3):
-    kernels.gemm_simt(a, b, c)
-    kernels.gemm_tc(a, b, c)                 # CTA-pair tf32
-    kernels.gemm_tc(a, b, c, mode=2)         # CTA-pair 3xBF16 (kind::f16)
-    kernels.gemm_tc(a, b, c, mode=0x100)     # single-CTA co-scheduling shape, tf32
+CO = 0x100
+for _ in range(reps_):
+    kernels.gemm_simt(a, b, c, mode=CO)      # in-task SIMT shape (blocked accumulation)
+    kernels.gemm_tc(a, b, c, mode=CO)        # single-CTA co-scheduling shape, tf32
+    kernels.gemm_tc(a, b, c, mode=2 | CO)    # co-scheduling shape, 3xBF16
+    kernels.gemm_tc(a, b, c)                 # CTA-pair tf32 (standalone)
     kernels.vote(reps[:2], 1e-3)
     kernels.vote(reps, 1e-3, voted=reps[0])
     kernels.checkpoint(dst, base)
