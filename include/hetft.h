@@ -130,6 +130,26 @@ int hf_vote_async(const void* const* replicas, int K, int64_t n, int dtype,
                   void* voted, hf_vote_result* dev_out, void* workspace,
                   int device, void* stream);
 
+/* Several votes in one launch: `count` items (any number; launched in
+ * groups of HF_VOTE_BATCH_MAX) sharing K, dtype and tolerances, each with
+ * its own replicas, size, optional voted buffer (== replicas[0]: in place),
+ * result (device or pinned host memory) and workspace (as for
+ * hf_vote_async; one per item in flight).  Asynchronous.  Small votes are
+ * bound by the per-launch host cost and each grid's ramp and tail; one
+ * shared grid amortises both (e.g. every output area of a task, or the
+ * votes of several tasks). */
+#define HF_VOTE_BATCH_MAX 32
+typedef struct hf_vote_item {
+    const void* replicas[HF_MAX_K];
+    int64_t n;
+    void* voted;
+    hf_vote_result* out;
+    void* workspace;
+} hf_vote_item;
+int hf_vote_batch(const hf_vote_item* items, int count, int K, int dtype,
+                  const double* rel_tol, const int32_t* ulp_tol,
+                  int device, void* stream);
+
 /* Integer areas of arbitrary element width (ValueType.INT, any width):
  * elements agree iff all `elem_width` bytes are equal. */
 int hf_vote_bytes(const void* const* replicas, int K, int64_t n, int elem_width,

@@ -40,7 +40,7 @@ HF_GEMM_COSCHEDULE = 0x100
 # every symbol include/hetft.h declares (checked by tests/test_capi.py)
 EXPORTED = (
     "hf_init", "hf_last_error", "hf_version", "hf_device_count", "hf_peer_enabled",
-    "hf_vote", "hf_vote_workspace_bytes", "hf_vote_workspace_init", "hf_vote_async",
+    "hf_vote", "hf_vote_workspace_bytes", "hf_vote_workspace_init", "hf_vote_async", "hf_vote_batch",
     "hf_vote_bytes", "hf_copy", "hf_fill", "hf_checkpoint", "hf_restore", "hf_checksum",
     "hf_inject_bitflip", "hf_inject_scale", "hf_scribble", "hf_gemm_tc", "hf_gemm_simt",
     "hf_debug_spin", "hf_vec_inc", "hf_vec_path",
@@ -58,6 +58,20 @@ class HfVoteResult(ctypes.Structure):
         ("reserved", ctypes.c_int32),
         ("first_raw0", ctypes.c_uint64),
         ("kernel_ns", ctypes.c_int64),
+    ]
+
+
+HF_VOTE_BATCH_MAX = 32
+
+
+class HfVoteItem(ctypes.Structure):
+    """hf_vote_item (include/hetft.h): one vote of an hf_vote_batch launch."""
+    _fields_ = [
+        ("replicas", ctypes.c_void_p * HF_MAX_K),
+        ("n", ctypes.c_int64),
+        ("voted", ctypes.c_void_p),
+        ("out", ctypes.c_void_p),
+        ("workspace", ctypes.c_void_p),
     ]
 
 
@@ -98,6 +112,8 @@ def _declare(lib):
         "hf_vote_workspace_init": (_i32, [_c_void_p, _i32, _c_void_p]),
         "hf_vote_async": (_i32, [P(_c_void_p), _i32, _i64, _i32, P(ctypes.c_double),
                                  P(ctypes.c_int32), _c_void_p, _c_void_p, _c_void_p, _i32, _c_void_p]),
+        "hf_vote_batch": (_i32, [P(HfVoteItem), _i32, _i32, _i32, P(ctypes.c_double), P(ctypes.c_int32), _i32,
+                                 _c_void_p]),
         "hf_vote_bytes": (_i32, [P(_c_void_p), _i32, _i64, _i32, _c_void_p, P(HfVoteResult), _i32,
                                  _c_void_p]),
         "hf_copy": (_i32, [_c_void_p, _i32, _c_void_p, _i32, _i64, _c_void_p]),

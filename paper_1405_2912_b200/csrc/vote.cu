@@ -311,8 +311,16 @@ __device__ __forceinline__ typename Elem<DT>::T vote_elem(const typename Elem<DT
     return out;
 }
 
-template <int DT, int K, int UNROLL>
-__global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteParams p) {
+// One vote over blocks [0, nblk) of a grid: the body of vote_kernel (one
+// vote per launch, blk = its block index) and of vote_batch_kernel (several
+// votes per launch, each over its own range of blocks).  `p` supplies the
+// pair predicates; the item's buffers, sizes and workspace are passed apart.
+// Item: rep(r), voted(), n(), nvec(), in_place(), ws(), out() — read from the
+// kernel's parameter space at each use (constant bank), as the one-vote
+// kernel always did, so they hold no registers across the streaming loop.
+template <int DT, int K, int UNROLL, typename Item>
+__device__ __forceinline__ void vote_body(const VoteParams& p, const Item& it, const unsigned blk,
+                                          const unsigned nblk) {
     using E = Elem<DT>;
     using T = typename E::T;
     constexpr int PV = E::kPerVec;
@@ -324,8 +332,8 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
     acc.first = ~0ull;
     acc.raw0 = 0;
 
-    const long long gtid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const long long gstride = static_cast<long long>(gridDim.x) * blockDim.x;
+    const long long gtid = static_cast<long long>(blk) * blockDim.x + threadIdx.x;
+    const long long gstride = static_cast<long long>(nblk) * blockDim.x;
 
     // Programmatic dependent launch: this grid may be resident before the
     // previous kernel of the stream has finished (its launch and CTA
@@ -336,19 +344,19 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
     // after the dependency wait .. the last CTA's finalisation
     // (block 0 is dispatched first; its thread 0 stores the reading with the
     // block's counts at the end, so the timer latency overlaps its loads)
-    const unsigned long long t_begin = (blockIdx.x == 0 && threadIdx.x == 0) ? globaltimer_ns() : 0ull;
+    const unsigned long long t_begin = (blk == 0 && threadIdx.x == 0) ? globaltimer_ns() : 0ull;
 
     // ---- vector loop: UNROLL x K 128-bit loads in flight per thread ----
     long long j = gtid;
-    for (; j + (UNROLL - 1) * gstride < p.nvec; j += UNROLL * gstride) {
+    for (; j + (UNROLL - 1) * gstride < it.nvec(); j += UNROLL * gstride) {
         uint4 v[UNROLL][K];
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u)
 #pragma unroll
             for (int r = 0; r < K; ++r)
-                v[u][r] = (K >= 3 && r == 0 && p.in_place)
-                              ? ld_stream_rw(reinterpret_cast<const uint4*>(p.rep[r]) + (j + u * gstride))
-                              : ld_stream(reinterpret_cast<const uint4*>(p.rep[r]) + (j + u * gstride));
+                v[u][r] = (K >= 3 && r == 0 && it.in_place())
+                              ? ld_stream_rw(reinterpret_cast<const uint4*>(it.rep(r)) + (j + u * gstride))
+                              : ld_stream(reinterpret_cast<const uint4*>(it.rep(r)) + (j + u * gstride));
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u) {
             const long long vj = j + u * gstride;
@@ -362,7 +370,7 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
                 o[e] = vote_elem<DT, K>(x, p, acc, static_cast<unsigned long long>(vj) * PV + e);
                 changed |= o[e] != x[0];
             }
-            if (p.voted != nullptr && (!p.in_place || changed)) {
+            if (it.voted() != nullptr && (!it.in_place() || changed)) {
                 uint4 w;
                 if constexpr (sizeof(T) == 4) {
                     w = make_uint4(o[0], o[1], o[2], o[3]);
@@ -384,17 +392,17 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
                                 (static_cast<uint32_t>(o[4 * q + 3]) << 24);
                     w = make_uint4(ww[0], ww[1], ww[2], ww[3]);
                 }
-                st_stream(reinterpret_cast<uint4*>(p.voted) + vj, w);
+                st_stream(reinterpret_cast<uint4*>(it.voted()) + vj, w);
             }
         }
     }
     // remainder vectors (fewer than UNROLL strides left)
-    for (; j < p.nvec; j += gstride) {
+    for (; j < it.nvec(); j += gstride) {
         uint4 v[K];
 #pragma unroll
         for (int r = 0; r < K; ++r)
-            v[r] = (K >= 3 && r == 0 && p.in_place) ? ld_stream_rw(reinterpret_cast<const uint4*>(p.rep[r]) + j)
-                                                    : ld_stream(reinterpret_cast<const uint4*>(p.rep[r]) + j);
+            v[r] = (K >= 3 && r == 0 && it.in_place()) ? ld_stream_rw(reinterpret_cast<const uint4*>(it.rep(r)) + j)
+                                                    : ld_stream(reinterpret_cast<const uint4*>(it.rep(r)) + j);
         T o[PV];
         bool changed = false;
 #pragma unroll
@@ -405,21 +413,21 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
             o[e] = vote_elem<DT, K>(x, p, acc, static_cast<unsigned long long>(j) * PV + e);
             changed |= o[e] != x[0];
         }
-        if (p.voted != nullptr && (!p.in_place || changed)) {
-            T* dst = reinterpret_cast<T*>(p.voted) + j * PV;
+        if (it.voted() != nullptr && (!it.in_place() || changed)) {
+            T* dst = reinterpret_cast<T*>(it.voted()) + j * PV;
 #pragma unroll
             for (int e = 0; e < PV; ++e) dst[e] = o[e];
         }
     }
     // ---- scalar tail (and the whole buffer when pointers are unaligned) ----
-    for (long long i = p.nvec * PV + gtid; i < p.n; i += gstride) {
+    for (long long i = it.nvec() * PV + gtid; i < it.n(); i += gstride) {
         T x[K];
 #pragma unroll
         for (int r = 0; r < K; ++r)
-            x[r] = (K >= 3 && r == 0 && p.in_place) ? reinterpret_cast<const volatile T*>(p.rep[r])[i]
-                                                    : __ldg(reinterpret_cast<const T*>(p.rep[r]) + i);
+            x[r] = (K >= 3 && r == 0 && it.in_place()) ? reinterpret_cast<const volatile T*>(it.rep(r))[i]
+                                                    : __ldg(reinterpret_cast<const T*>(it.rep(r)) + i);
         T o = vote_elem<DT, K>(x, p, acc, static_cast<unsigned long long>(i));
-        if (p.voted != nullptr && (!p.in_place || o != x[0])) reinterpret_cast<T*>(p.voted)[i] = o;
+        if (it.voted() != nullptr && (!it.in_place() || o != x[0])) reinterpret_cast<T*>(it.voted())[i] = o;
     }
 
     // the next kernel of the stream may start launching while this grid reduces
@@ -452,14 +460,14 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
         if (lane == 0) atomicMin(&s_first, f);
     }
     __shared__ unsigned long long s_fd, s_t0;
-    if (blockIdx.x == 0 && threadIdx.x == 0) s_t0 = t_begin;   // for whichever thread leads the epilogue
+    if (blk == 0 && threadIdx.x == 0) s_t0 = t_begin;   // for whichever thread leads the epilogue
     __syncthreads();
     // the block's epilogue thread: for K >= 3 the one holding the block's
     // first divergence (element indices are unique per thread) so it can
     // publish replica 0's value there without another barrier, else thread 0
     const bool leader = (K >= 3 && s_first != ~0ull) ? acc.first == s_first : threadIdx.x == 0;
     if (leader) {
-        VoteWorkspace* ws = p.ws;
+        VoteWorkspace* ws = it.ws();
 #pragma unroll
         for (int r = 0; r <= K; ++r) {
             unsigned long long c = s_cnt[r];
@@ -468,14 +476,14 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
         if (s_first != ~0ull) {
             atomicMin(&ws->first_div, s_first);
             if (K >= 3) {
-                ws->blk_first[blockIdx.x] = s_first;
-                ws->blk_raw0[blockIdx.x] = static_cast<unsigned long long>(acc.raw0);
+                ws->blk_first[blk] = s_first;
+                ws->blk_raw0[blk] = static_cast<unsigned long long>(acc.raw0);
             }
         }
-        if (blockIdx.x == 0) ws->t_start = s_t0;
+        if (blk == 0) ws->t_start = s_t0;
         __threadfence();
         unsigned int t = atomicAdd(&ws->ticket, 1u);
-        s_last = (t == gridDim.x - 1);
+        s_last = (t == nblk - 1);
         if (s_last) {
             __threadfence();
             s_fd = *(volatile unsigned long long*)&ws->first_div;
@@ -485,17 +493,17 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
     // ---- last block: finalise the result and re-arm the workspace ----------
     if (K >= 3 && s_last && s_fd != ~0ull) {
         // whose record is the global minimum (then re-arm them all)
-        volatile unsigned long long* bf = p.ws->blk_first;
-        for (unsigned int b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
-            if (bf[b] == s_fd) s_raw0 = p.ws->blk_raw0[b];
+        volatile unsigned long long* bf = it.ws()->blk_first;
+        for (unsigned int b = threadIdx.x; b < nblk; b += blockDim.x) {
+            if (bf[b] == s_fd) s_raw0 = it.ws()->blk_raw0[b];
             bf[b] = ~0ull;
         }
         __syncthreads();
     }
     if (s_last && threadIdx.x == 0) {
         const unsigned long long t_end = globaltimer_ns();   // latency overlaps the reads below
-        VoteWorkspace* ws = p.ws;
-        hf_vote_result* out = p.out;
+        VoteWorkspace* ws = it.ws();
+        hf_vote_result* out = it.out();
         volatile unsigned long long* vm = ws->mismatch;
         long long best = -1;
         int winner = 0;
@@ -528,6 +536,63 @@ __global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteP
         __threadfence();
         ws->ticket = 0;
     }
+}
+
+struct OneVote {
+    const VoteParams& p;
+    __device__ const uint8_t* rep(int r) const { return p.rep[r]; }
+    __device__ uint8_t* voted() const { return p.voted; }
+    __device__ long long n() const { return p.n; }
+    __device__ long long nvec() const { return p.nvec; }
+    __device__ int in_place() const { return p.in_place; }
+    __device__ VoteWorkspace* ws() const { return p.ws; }
+    __device__ hf_vote_result* out() const { return p.out; }
+};
+
+template <int DT, int K, int UNROLL>
+__global__ void __launch_bounds__(256) vote_kernel(const __grid_constant__ VoteParams p) {
+    vote_body<DT, K, UNROLL>(p, OneVote{p}, blockIdx.x, gridDim.x);
+}
+
+// Several votes in one launch (hf_vote_batch): same K, dtype and tolerances,
+// each item over its own contiguous range of blocks (sized by its bytes),
+// its own workspace, result and last-block finalisation.  One launch
+// instead of `count`: small votes (<= tens of MiB) are bound by the host's
+// launch cost (~7-9 us per call) and by each grid's ramp and tail, which a
+// shared grid overlaps.
+constexpr int kMaxBatch = HF_VOTE_BATCH_MAX;
+struct VoteBatchParams {
+    VoteParams pred;                       // pair predicates (item fields unused)
+    int count;
+    int blk_begin[kMaxBatch + 1];
+    const uint8_t* rep[kMaxBatch][HF_MAX_K];
+    uint8_t* voted[kMaxBatch];
+    long long n[kMaxBatch];
+    long long nvec[kMaxBatch];
+    hf_vote_result* out[kMaxBatch];
+    VoteWorkspace* ws[kMaxBatch];
+    int in_place[kMaxBatch];
+};
+
+struct BatchItem {
+    const VoteBatchParams& bp;
+    int i;
+    __device__ const uint8_t* rep(int r) const { return bp.rep[i][r]; }
+    __device__ uint8_t* voted() const { return bp.voted[i]; }
+    __device__ long long n() const { return bp.n[i]; }
+    __device__ long long nvec() const { return bp.nvec[i]; }
+    __device__ int in_place() const { return bp.in_place[i]; }
+    __device__ VoteWorkspace* ws() const { return bp.ws[i]; }
+    __device__ hf_vote_result* out() const { return bp.out[i]; }
+};
+
+template <int DT, int K, int UNROLL>
+__global__ void __launch_bounds__(256) vote_batch_kernel(const __grid_constant__ VoteBatchParams bp) {
+    int i = 0;
+    while (i + 1 < bp.count && static_cast<int>(blockIdx.x) >= bp.blk_begin[i + 1]) ++i;
+    const unsigned b0 = static_cast<unsigned>(bp.blk_begin[i]);
+    vote_body<DT, K, UNROLL>(bp.pred, BatchItem{bp, i}, blockIdx.x - b0,
+                             static_cast<unsigned>(bp.blk_begin[i + 1]) - b0);
 }
 
 // Arbitrary-width integer areas (ValueType.INT with width not in {1,2,4,8}):
@@ -653,6 +718,13 @@ __global__ void ws_init_kernel(VoteWorkspace* ws) {
     ws->t_start = ~0ull;
 }
 
+#define HF_VOTE_B(DT) (const void*)vote_batch_kernel<DT, 2, 2>, (const void*)vote_batch_kernel<DT, 3, 2>, \
+    (const void*)vote_batch_kernel<DT, 4, 2>, (const void*)vote_batch_kernel<DT, 5, 2>, \
+    (const void*)vote_batch_kernel<DT, 6, 1>, (const void*)vote_batch_kernel<DT, 7, 1>, \
+    (const void*)vote_batch_kernel<DT, 8, 1>
+static const int kRegisteredBatch = register_kernels({HF_VOTE_B(HF_F32), HF_VOTE_B(HF_F64), HF_VOTE_B(HF_U8),
+                                                      HF_VOTE_B(HF_U16), HF_VOTE_B(HF_U32), HF_VOTE_B(HF_U64)});
+#undef HF_VOTE_B
 #define HF_VOTE_K(DT) (const void*)vote_kernel<DT, 2, 2>, (const void*)vote_kernel<DT, 3, 2>, \
     (const void*)vote_kernel<DT, 4, 2>, (const void*)vote_kernel<DT, 5, 2>, (const void*)vote_kernel<DT, 6, 1>, \
     (const void*)vote_kernel<DT, 7, 1>, (const void*)vote_kernel<DT, 8, 1>
@@ -812,6 +884,85 @@ static int launch_vote(VoteParams& p, int K, int dtype, int width, int device, c
     return HF_OK;
 }
 
+using VoteBatchKernel = void (*)(VoteBatchParams);
+
+template <int DT>
+static VoteBatchKernel pick_batch(int K) {
+    switch (K) {
+        case 2: return vote_batch_kernel<DT, 2, 2>;
+        case 3: return vote_batch_kernel<DT, 3, 2>;
+        case 4: return vote_batch_kernel<DT, 4, 2>;
+        case 5: return vote_batch_kernel<DT, 5, 2>;
+        case 6: return vote_batch_kernel<DT, 6, 1>;
+        case 7: return vote_batch_kernel<DT, 7, 1>;
+        case 8: return vote_batch_kernel<DT, 8, 1>;
+        default: return nullptr;
+    }
+}
+
+static VoteBatchKernel select_batch(int dtype, int K) {
+    switch (dtype) {
+        case HF_F32: return pick_batch<HF_F32>(K);
+        case HF_F64: return pick_batch<HF_F64>(K);
+        case HF_U8: return pick_batch<HF_U8>(K);
+        case HF_U16: return pick_batch<HF_U16>(K);
+        case HF_U32: return pick_batch<HF_U32>(K);
+        case HF_U64: return pick_batch<HF_U64>(K);
+        default: return nullptr;
+    }
+}
+
+// Up to kMaxBatch items in one grid.  The grid is one wave of resident CTAs
+// (as for a single vote); an item gets blocks in proportion to its bytes,
+// at least one and at most what it can use, so small items finish in one
+// pass while the large ones stream.
+static int launch_vote_batch(const hf_vote_item* items, int count, int K, int dtype, const double* rel_tol,
+                             const int32_t* ulp_tol, int device, cudaStream_t st) {
+    VoteBatchKernel k = select_batch(dtype, K);
+    HF_REQUIRE(k != nullptr, "hf_vote_batch: unsupported dtype %d / K %d", dtype, K);
+    const int width = elem_size(dtype);
+    static VoteBatchParams bp;      // ~5 KB: built under the lock, copied into the launch
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    memset(&bp, 0, sizeof(bp));
+    long long work[kMaxBatch], total = 0;
+    for (int i = 0; i < count; ++i) {
+        HF_REQUIRE(items[i].out != nullptr && items[i].workspace != nullptr,
+                   "hf_vote_batch: item %d has a NULL result/workspace", i);
+        HF_REQUIRE(items[i].n > 0, "hf_vote_batch: item %d has n <= 0", i);
+        VoteParams p;
+        int rc = fill_params(p, items[i].replicas, K, items[i].n, width, rel_tol, ulp_tol, items[i].voted);
+        if (rc) return rc;
+        if (i == 0) bp.pred = p;            // the pair predicates are the same for every item
+        for (int r = 0; r < K; ++r) bp.rep[i][r] = p.rep[r];
+        bp.voted[i] = p.voted;
+        bp.n[i] = p.n;
+        bp.nvec[i] = p.nvec;
+        bp.in_place[i] = p.in_place;
+        bp.out[i] = items[i].out;
+        bp.ws[i] = static_cast<VoteWorkspace*>(items[i].workspace);
+        work[i] = p.nvec > 0 ? p.nvec : p.n;
+        total += work[i];
+    }
+    const int threads = 256;
+    long long cap = static_cast<long long>(num_sms(device)) * resident_ctas(reinterpret_cast<const void*>(k), device);
+    int b = 0;
+    for (int i = 0; i < count; ++i) {
+        long long want = (work[i] + threads - 1) / threads;
+        long long share = static_cast<long long>(static_cast<double>(cap) * work[i] / total);
+        long long nb = want < share ? want : share;
+        if (nb < 1) nb = 1;
+        if (nb > kMaxVoteBlocks) nb = kMaxVoteBlocks;
+        bp.blk_begin[i] = b;
+        b += static_cast<int>(nb);
+    }
+    bp.blk_begin[count] = b;
+    bp.count = count;
+    HF_CUDA_CHECK(launch_pdl(k, dim3(b), dim3(threads), 0, st, bp));
+    HF_CHECK_LAUNCH();
+    return HF_OK;
+}
+
 // Per-device pool of (workspace, device result) slots for the synchronous API.
 struct SyncSlot {
     VoteWorkspace* ws = nullptr;
@@ -918,6 +1069,21 @@ int hf_vote_workspace_init(void* workspace, int device, void* stream) {
     HF_REQUIRE(g.ok, "hf_vote_workspace_init: cannot select device %d", device);
     hf::ws_init_kernel<<<1, 256, 0, hf::as_stream(stream)>>>(static_cast<hf::VoteWorkspace*>(workspace));
     HF_CHECK_LAUNCH();
+    return HF_OK;
+}
+
+int hf_vote_batch(const hf_vote_item* items, int count, int K, int dtype, const double* rel_tol,
+                  const int32_t* ulp_tol, int device, void* stream) {
+    HF_REQUIRE(items != nullptr && count >= 0, "hf_vote_batch: bad items/count");
+    HF_REQUIRE(hf::elem_size(dtype) > 0, "hf_vote_batch: unknown dtype %d", dtype);
+    if (count == 0) return HF_OK;
+    hf::DeviceGuard g(device);
+    HF_REQUIRE(g.ok, "hf_vote_batch: cannot select device %d", device);
+    for (int i0 = 0; i0 < count; i0 += hf::kMaxBatch) {
+        const int c = count - i0 < hf::kMaxBatch ? count - i0 : hf::kMaxBatch;
+        int rc = hf::launch_vote_batch(items + i0, c, K, dtype, rel_tol, ulp_tol, device, hf::as_stream(stream));
+        if (rc) return rc;
+    }
     return HF_OK;
 }
 

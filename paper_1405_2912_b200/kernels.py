@@ -196,6 +196,53 @@ def vote_async(replicas: Sequence[torch.Tensor], ws: VoteWorkspace, rel_tol=0.00
     _count()
 
 
+class VoteBatch:
+    """A prepared hf_vote_batch launch: the descriptor array (replica, voted,
+    result and workspace pointers per vote) is built once, so repeated
+    launches over the same buffers cost one C call.  items: (replicas, voted
+    or None, VoteWorkspace, result tensor or None) per vote; every item has
+    the same K and dtype and shares the tolerances.  Results go to the given
+    tensor (device or pinned host, sizeof HfVoteResult bytes) or to the
+    workspace's device result; read them with VoteResult.from_c after the
+    stream passes the launch."""
+
+    def __init__(self, items: Sequence[tuple], rel_tol=0.001, ulp_tol=None, device: Optional[int] = None):
+        if not items:
+            raise ValueError("vote_batch: no items")
+        K = len(items[0][0])
+        dt = items[0][0][0].dtype
+        arr = (_lib.HfVoteItem * len(items))()
+        for it, (reps, voted, ws, out) in zip(arr, items):
+            if len(reps) != K or any(r.dtype != dt or r.numel() != reps[0].numel() or not r.is_contiguous()
+                                     for r in reps):
+                raise ValueError("vote_batch: every item needs K contiguous replicas of one size and dtype")
+            for r, t in enumerate(reps):
+                it.replicas[r] = t.data_ptr()
+            it.n = reps[0].numel()
+            it.voted = voted.data_ptr() if voted is not None else None
+            it.out = (out if out is not None else ws.result).data_ptr()
+            it.workspace = ws.ws.data_ptr()
+        self._items = list(items)          # keeps every buffer alive as long as the descriptors
+        self._arr = arr
+        self.K, self.count = K, len(items)
+        self._dtype = hf_dtype(items[0][0][0])
+        self.device = _dev(items[0][0][0]) if device is None else device
+        self._rel, self._ulp = _tolerances(K, rel_tol, ulp_tol)
+        self._lib = _lib.load()
+
+    def launch(self, stream: Optional[torch.cuda.Stream] = None) -> None:
+        check("hf_vote_batch", self._lib.hf_vote_batch(self._arr, self.count, self.K, self._dtype, self._rel,
+                                                       self._ulp, self.device, _stream_ptr(self.device, stream)))
+        _count(-(-self.count // _lib.HF_VOTE_BATCH_MAX))
+
+
+def vote_batch(items: Sequence[tuple], rel_tol=0.001, ulp_tol=None, device: Optional[int] = None,
+               stream: Optional[torch.cuda.Stream] = None) -> None:
+    """Several K-replica votes in one launch (hf_vote_batch); see VoteBatch."""
+    if items:
+        VoteBatch(items, rel_tol, ulp_tol, device).launch(stream)
+
+
 class _SliceSlot:
     """Per-device workspace + pinned host mirror for one in-flight slice."""
 

@@ -518,3 +518,58 @@ np.savez(sys.argv[1], voted=voted.cpu().numpy(), dst=dst.cpu().numpy(), inc=inc.
             outs.append(np.load(f))
         for key in ("voted", "dst", "inc", "res"):
             assert outs[0][key].tobytes() == outs[1][key].tobytes(), key
+
+
+@pytest.mark.parametrize("Kr,dtype", [(2, np.float32), (3, np.float32), (5, np.float32), (3, np.float64),
+                                      (3, np.uint16), (4, np.uint64)])
+def test_vote_batch_matches_single_votes(K, Kr, dtype):
+    """hf_vote_batch: 40 votes in two launches (32 + 8 items) of mixed sizes —
+    one element, ragged tails, a sub-vector item, an unaligned item, 4 MiB,
+    in place and not, with and without faults — every item's result
+    (verdict, counts, unresolved, first divergence, winner, replica 0's
+    value there) and voted bytes equal the oracle's; results land in pinned
+    host slots."""
+    import ctypes
+    from paper_1405_2912_b200 import _lib
+    rng = np.random.default_rng(Kr * 10 + np.dtype(dtype).itemsize)
+    sizes = [1, 3, 4, 5, 17, 1000, 4099, (1 << 20) + 3, 1 << 20] + [int(rng.integers(1, 70000)) for _ in range(31)]
+    items, expect, keep = [], [], []
+    for idx, n in enumerate(sizes):
+        if np.dtype(dtype).kind == "f":
+            base = rng.uniform(1, 2, n).astype(dtype)
+            reps = [(base * (1 + 1e-6 * rng.standard_normal(n))).astype(dtype) for _ in range(Kr)]
+        else:
+            base = rng.integers(0, np.iinfo(dtype).max, n, dtype=dtype)
+            reps = [base.copy() for _ in range(Kr)]
+        for f in range(idx % 4):                     # 0..3 faults in distinct replicas
+            r, e = (f + idx) % Kr, int(rng.integers(0, n))
+            reps[r].view(np.uint8)[e * reps[r].itemsize + reps[r].itemsize - 1] ^= 0x40
+        ores = ovote.vote(reps, 1e-3)
+        ts = [dev(x) for x in reps]
+        if idx == 5:                                  # unaligned replicas (scalar path)
+            ts = [torch.cat([torch.zeros(1, dtype=t.dtype, device="cuda"), t])[1:] for t in ts]
+        in_place = Kr >= 3 and idx % 2 == 0
+        voted = ts[0] if in_place else (torch.empty_like(ts[0]) if idx % 3 == 0 else None)
+        ws = K.VoteWorkspace(0)
+        out = torch.zeros(ctypes.sizeof(_lib.HfVoteResult), dtype=torch.uint8).pin_memory()
+        items.append((ts, voted, ws, out))
+        expect.append((ores, reps[0], voted))
+        keep.append(ts)
+    K.vote_batch(items, 1e-3)
+    torch.cuda.synchronize()
+    for (ts, voted, ws, out), (ores, rep0, vbuf) in zip(items, expect):
+        res = K.VoteResult.from_c(_lib.HfVoteResult.from_buffer_copy(out.numpy().tobytes()))
+        check_vote(res, ores, vbuf)
+        if Kr >= 3 and res.first_div >= 0:
+            w = rep0.itemsize
+            assert res.first_raw0 == int.from_bytes(rep0.view(np.uint8)[res.first_div * w:(res.first_div + 1) * w]
+                                                    .tobytes(), "little")
+        assert res.kernel_ns > 0
+
+
+def test_vote_batch_rejects_mixed_items(K):
+    ws = K.VoteWorkspace(0)
+    a = [torch.rand(100, device="cuda") for _ in range(3)]
+    b = [torch.rand(100, device="cuda") for _ in range(2)]
+    with pytest.raises(ValueError):
+        K.vote_batch([(a, None, ws, None), (b, None, ws, None)])

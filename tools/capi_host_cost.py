@@ -31,7 +31,16 @@ def t(name, fn, n_=100):
     return name, round(dt, 2)
 
 
+import ctypes
+reps = [torch.rand(1 << 18, device="cuda") for _ in range(3)]
+ws = kernels.VoteWorkspace(0, stream=st)
+res_host = torch.empty(ctypes.sizeof(_lib.HfVoteResult), dtype=torch.uint8).pin_memory()
+rptr = (ctypes.c_void_p * 3)(*[r.data_ptr() for r in reps])
+tol = (ctypes.c_double * 3)(1e-3, 1e-3, 1e-3)
 rows = [
+    t("hf_vote_async raw (K=3, 1 MiB)", lambda: lib.hf_vote_async(rptr, 3, 1 << 18, _lib.HF_F32, tol, None, None,
+                                                                   res_host.data_ptr(), ws.ws.data_ptr(), 0, sp)),
+    t("kernels.vote_async (K=3, 1 MiB)", lambda: kernels.vote_async(reps, ws, 1e-3, stream=st, result_into=res_host)),
     t("hf_gemm_tc raw (cosched)", lambda: lib.hf_gemm_tc(a.data_ptr(), b.data_ptr(), c.data_ptr(), n, n, n, CS, 0, sp)),
     t("hf_gemm_tc raw (plain)", lambda: lib.hf_gemm_tc(a.data_ptr(), b.data_ptr(), c.data_ptr(), n, n, n, 0, 0, sp)),
     t("hf_gemm_tc raw 3xtf32 cosched", lambda: lib.hf_gemm_tc(a.data_ptr(), b.data_ptr(), c.data_ptr(), n, n, n, CS | 1, 0, sp)),
