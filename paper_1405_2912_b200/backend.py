@@ -53,6 +53,7 @@ class CudaBackend:
         self.launches = 0             # libhetft kernel launches issued through this backend
         self.slice_across_gpus = True  # replicas on >= 2 GPUs: sliced vote
         self._vote_slots: dict = {}
+        self._event_pool: dict = {}        # device -> idle timing events
         self._tl = threading.local()
 
     # -- streams / timing ---------------------------------------------------------
@@ -154,26 +155,45 @@ class CudaBackend:
         kernels.copy(dst_host, src, stream=cs)
         return self.record(cs)
 
+    def _timing_event(self, device):
+        with self._lock:
+            pool = self._event_pool.get(device)
+            if pool:
+                return pool.pop()
+        return torch.cuda.Event(enable_timing=True)
+
     def timer_start(self, stream, device):
         if stream is None:
             import time
             return ("host", time.perf_counter_ns())
-        ev = torch.cuda.Event(enable_timing=True)
+        ev = self._timing_event(device)
         ev.record(stream)
         return ("cuda", ev)
 
-    def timer_stop(self, start, stream, device):
+    def timer_stop(self, start, stream, device, recycle: bool = True):
+        """Returns elapsed(): waits for the stop event and returns ns.  With
+        recycle, elapsed() hands both events back to the device's pool (four
+        fresh events per voted task cost ~10 us of host time); timers whose
+        stop event is exported as a readiness event (votes) must not recycle.
+        An abandoned timer (a hung attempt) keeps its events."""
         kind, t0 = start
         if kind == "host":
             import time
             dt = time.perf_counter_ns() - t0
             return lambda: dt
-        ev = torch.cuda.Event(enable_timing=True)
+        ev = self._timing_event(device)
         ev.record(stream)
+        pool = self._event_pool.setdefault(device, []) if recycle else None
+        lock = self._lock
 
         def elapsed() -> int:
             ev.synchronize()
-            return int(t0.elapsed_time(ev) * 1e6)
+            ns = int(t0.elapsed_time(ev) * 1e6)
+            if pool is not None:
+                with lock:
+                    if len(pool) < 256:
+                        pool.extend((t0, ev))
+            return ns
         elapsed.start_event = t0       # the executor's watchdog polls these
         elapsed.stop_event = ev
         return elapsed
@@ -357,7 +377,7 @@ class CudaBackend:
         kernels.vote_async([b.view(dt) for b in bufs], slot.ws, rel_tol, ulp_tol,
                            voted=voted.view(dt) if voted is not None else None, stream=st,
                            result_into=slot.host)
-        stop = self.timer_stop(start, st, device)
+        stop = self.timer_stop(start, st, device, recycle=False)
         self.launches += 1
         return _PendingVote(self, slot, device, stop)
 
@@ -400,7 +420,7 @@ class CudaBackend:
             parts.append((lo, d, slot))
         for d in devs[1:]:
             streams[lead].wait_stream(streams[d])
-        stop = self.timer_stop(start, streams[lead], lead)
+        stop = self.timer_stop(start, streams[lead], lead, recycle=False)
         return _PendingSliced(self, parts, K, stop)
 
     def prewarm(self, devices, vote_slots: int = 4) -> None:
@@ -453,7 +473,7 @@ class CudaBackend:
                                       devices=devs, streams=streams)
             for d in devs[1:]:
                 streams[devs[0]].wait_stream(streams[d])
-            stop = self.timer_stop(start, streams[devs[0]], devs[0])
+            stop = self.timer_stop(start, streams[devs[0]], devs[0], recycle=False)
             self.launches += len(devs)
             ns = stop()
             return res, (res.kernel_ns or ns)
@@ -469,7 +489,7 @@ class CudaBackend:
             views = [b.view(dt) for b in bufs]
             res = kernels.vote(views, rel_tol, ulp_tol, voted=voted.view(dt) if voted is not None else None,
                                device=device, stream=st)
-        stop = self.timer_stop(start, st, device)
+        stop = self.timer_stop(start, st, device, recycle=False)
         self.launches += 1
         ns = stop()
         return res, (getattr(res, "kernel_ns", 0) or ns)

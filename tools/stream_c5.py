@@ -13,7 +13,9 @@ invalidated and the retry restores A and B from the checkpoint).
 
 Every committed C is verified on the GPU against the binary64 product of its
 inputs (an hf_vote K = 2 under the task's δ must return "match"), inside the
-timed region, so the rate includes that check.  There is no data-path
+timed region, so the rate includes that check; the checks run asynchronously
+on the compute stream (a ring of pinned result slots, read when a slot comes
+round again and before the timed region closes).  There is no data-path
 collective: ranks meet only for the barrier, the max of the device times and
 the sum of the counters (NCCL).
 
@@ -26,6 +28,7 @@ Writes one JSON line (rank 0) to stdout and, with --out, to a file.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import sys
@@ -57,7 +60,7 @@ def main():
     args = parse()
     import torch.distributed as dist
     import paper_1405_2912_b200 as hf
-    from paper_1405_2912_b200 import kernels, sharding
+    from paper_1405_2912_b200 import _lib, kernels, sharding
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -102,10 +105,31 @@ def main():
            "timeouts": 0, "vote_mismatch": 0, "votes_match": 0, "votes_corrected": 0, "votes_mismatch": 0,
            "verify_fail": 0}
 
+    # verification of every committed C against its binary64 product, on the
+    # GPU and asynchronous: hf_vote_async on the runtime's compute stream
+    # (ordered after the task's vote; the caching allocator cannot reuse C
+    # before it), results into a ring of pinned slots checked when a slot
+    # comes round again and at the end — no host sync per task
+    vstream = rt.backend.stream(dev)
+    ring = [(kernels.VoteWorkspace(dev, stream=vstream),
+             torch.empty(ctypes.sizeof(_lib.HfVoteResult), dtype=torch.uint8).pin_memory()) for _ in range(64)]
+    pending = {}
+
+    def check_slot(i):
+        ev = pending.pop(i, None)
+        if ev is not None:
+            ev.synchronize()
+            r = kernels.VoteResult.from_c(_lib.HfVoteResult.from_buffer_copy(ring[i][1].numpy().tobytes()))
+            cnt["verify_fail"] += int(r.verdict != "match")
+
     def account(rep, j, ic):
         c = rt.read_tensor(ic).view(torch.float32)
-        ok = kernels.vote([c, refs[j]], 1e-3).verdict == "match"
-        cnt["verify_fail"] += int(not ok)
+        i = cnt["tasks"] % len(ring)
+        check_slot(i)
+        kernels.vote_async([c, refs[j]], ring[i][0], 1e-3, stream=vstream, result_into=ring[i][1])
+        ev = torch.cuda.Event()
+        ev.record(vstream)
+        pending[i] = ev
         cnt["tasks"] += 1
         cnt["rounds"] += rep.rounds
         cnt["attempts"] += rep.attempts
@@ -141,6 +165,9 @@ def main():
                 rt.release(x)
 
     run(range(args.warmup), False)
+    for i in list(pending):
+        check_slot(i)
+    cnt["verify_fail"] = 0
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -149,6 +176,8 @@ def main():
     w0 = time.perf_counter()
     e0.record(st)
     run(mine, True)
+    for i in list(pending):
+        check_slot(i)
     e1.record(st)
     torch.cuda.synchronize()
     wall = time.perf_counter() - w0
