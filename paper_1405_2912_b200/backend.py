@@ -423,6 +423,37 @@ class CudaBackend:
         stop = self.timer_stop(start, streams[lead], lead, recycle=False)
         return _PendingSliced(self, parts, K, stop)
 
+    def vote_start_batch(self, specs: Sequence, rel_tol, device: Optional[int] = None) -> list:
+        """Several votes (e.g. every output area of one task) in one
+        hf_vote_batch launch.  specs: (replicas, value type, width, ulp_tol,
+        voted) per vote.  Falls back to one vote_start each unless every vote
+        is typed, has the same element type, K and ULP rule, and all replicas
+        sit on one GPU.  Returns one pending handle per spec."""
+        def single():
+            return [self.vote_start(b, vt, w, rel_tol, u, voted=v, device=device) for b, vt, w, u, v in specs]
+        devs, dts = set(), set()
+        for bufs, vt, width, ulps, _v in specs:
+            if not (vt.numpy_dtype is not None or width in INT_DTYPES):
+                return single()
+            dts.add((view_dtype(vt, width), len(bufs), None if ulps is None else tuple(ulps)))
+            for b in bufs:
+                if b.device.type != "cuda":
+                    return single()
+                devs.add(b.device.index)
+        if len(devs) != 1 or len(dts) != 1:
+            return single()
+        dev = devs.pop()
+        st = self.stream(dev)
+        dt = torch_dtype(dts.pop()[0])
+        slots = [self._vote_slot(dev) for _ in specs]
+        items = [([b.view(dt) for b in bufs], v.view(dt) if v is not None else None, slot.ws, slot.host)
+                 for (bufs, _vt, _w, _u, v), slot in zip(specs, slots)]
+        start = self.timer_start(st, dev)
+        kernels.VoteBatch(items, rel_tol, specs[0][3], device=dev).launch(st)
+        stop = self.timer_stop(start, st, dev, recycle=False)
+        self.launches += 1
+        return [_PendingVote(self, slot, dev, stop) for slot in slots]
+
     def prewarm(self, devices, vote_slots: int = 4) -> None:
         """Create each device's compute stream and a few vote result slots up
         front.  A slot holds pinned host memory, and the first cudaHostAlloc of

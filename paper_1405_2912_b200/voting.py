@@ -178,16 +178,24 @@ def vote_buffers_start(backend, areas: Sequence[tuple], rel_tols: Sequence[float
     order = list(range(K)) if order is None else list(order)
     if sorted(order) != list(range(K)):
         raise DispatchError(f"replica order {order} is not a permutation of 0..{K - 1}")
-    pending = []
     for area, bufs, vt, width in areas:
         if len(bufs) != K:
             raise DispatchError(f"area {area!r}: {len(bufs)} replicas, expected {K}")
+    rels = [rel_tols[i] for i in order]
+    specs = []
+    for area, bufs, vt, width in areas:
         seen = [bufs[i] for i in order]
         ulps = None if ulp is None or vt.numpy_dtype is None else [ulp] * K
-        h = backend.vote_start(seen, vt, width, [rel_tols[i] for i in order], ulps,
-                               voted=seen[0] if (in_place and K >= 3) else None, device=device)
-        pending.append((area, bufs, vt, width, h, order))
-    return pending
+        specs.append((seen, vt, width, ulps, seen[0] if (in_place and K >= 3) else None))
+    batch = getattr(backend, "vote_start_batch", None)
+    if batch is not None and len(specs) > 1:
+        # every output area of the task in one launch (hf_vote_batch) when
+        # the backend can: same K, element type and tolerances, one device
+        handles = batch(specs, rels, device=device)
+    else:
+        handles = [backend.vote_start(seen, vt, width, rels, ulps, voted=v, device=device)
+                   for seen, vt, width, ulps, v in specs]
+    return [(area, bufs, vt, width, h, order) for (area, bufs, vt, width), h in zip(areas, handles)]
 
 
 def vote_buffers_finish(backend, pending: list) -> VoteOutcome:

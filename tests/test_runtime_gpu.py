@@ -462,3 +462,69 @@ def test_task_stream_hang_redispatches_to_another_gpu():
     assert rep.success and rep.fault_counts["timeout"] == 1
     assert np.array_equal(rt.read_array(out), data)
     assert rep.committed.unit_id.startswith("g1.")
+
+
+TWO_OUT_PARAMS = (hf.Param.area("input", "r"), hf.Param.area("out_a", "w"), hf.Param.area("out_b", "w"),
+                  hf.Param.scalar("count"))
+
+
+def _two_out_body(ctx):
+    src = ctx.request("input", "r")
+    kernels.copy(ctx.request("out_a", "w"), src, stream=ctx.stream)
+    kernels.vec_inc(src, ctx.request("out_b", "w"), stream=ctx.stream)
+
+
+def test_multi_area_task_votes_in_one_batch_launch():
+    """A task with two output areas: the executor votes both in one
+    hf_vote_batch launch (CudaBackend.vote_start_batch).  Every round's
+    fault placement (which write view, element, bit: reference draw order)
+    and the combined decision — sorted-area order, counts summed over areas,
+    first divergence from the first diverging area (voting.py:106-123) —
+    equal the oracle replay."""
+    K, n = 3, 5003
+    kinds = [f"gpu-v{i}" for i in range(K)]
+    cfg = {"memory_spaces": [{"id": "host", "host": True}, {"id": "gpu0mem", "device": 0}],
+           "units": [{"id": f"u{i}", "kind": kinds[i], "memory_space": "gpu0mem", "timing": "measured",
+                      "corrupt_prob": 0.4, "corrupt_mode": "bitflip", "seed": 900 + i} for i in range(K)]}
+    rt = hf.Runtime(hf.load_fleet(cfg), hf.RuntimeConfig(serial_replicas=True, attempt_limit=200))
+    task = rt.declare_task("two", TWO_OUT_PARAMS)
+    for i in range(K):
+        rt.attach_kernel(task, f"k{i}", kinds[i], _two_out_body)
+    launches = []
+    orig = rt.backend.vote_start_batch
+
+    def spy(specs, rel, device=None):
+        launches.append(len(specs))
+        return orig(specs, rel, device=device)
+    rt.backend.vote_start_batch = spy
+    rng = np.random.default_rng(4)
+    rngs = {f"u{i}": random.Random(900 + i) for i in range(K)}
+    for t in range(12):
+        data = rng.uniform(1, 2, n).astype(np.float32)
+        inp = rt.register_data(data.tobytes(), n, hf.ValueType.FLOAT32, "r")
+        oa = rt.register_data(bytes(4 * n), n, hf.ValueType.FLOAT32, "w")
+        ob = rt.register_data(bytes(4 * n), n, hf.ValueType.FLOAT32, "w")
+        rep = rt.invoke(task, {"input": inp, "out_a": oa, "out_b": ob, "count": n}, hf.Strategy(hf.StrategyKind.HET_TMR))
+        assert rep.success
+        for log in rep.rounds_log:
+            views = {}
+            for slot, unit in sorted(log["launched"].items()):
+                va, vb = data.copy(), (data + np.float32(1)).astype(np.float32)
+                fault_schedule.apply_attempt(rngs[unit], (0, 0, 0, 0.4), [va, vb], [True, True], mode="bitflip")
+                views[slot] = (va, vb)
+            if "verdict" not in log:
+                continue
+            per = {}
+            for ai, area in enumerate((oa, ob)):
+                per[area] = ovote.vote([views[s][ai] for s in range(K)], 1e-3)
+            mism = [sum(per[a].mismatch[r] for a in per) for r in range(K)]
+            unres = sum(per[a].unresolved for a in per)
+            verdict = "mismatch" if unres else ("corrected" if any(mism) else "match")
+            assert (log["verdict"], log["mismatch"], log["unresolved"]) == (verdict, mism, unres)
+            firsts = [(a, per[a].first_div) for a in sorted(per) if per[a].first_div >= 0]
+            fd = log["first_divergence"]
+            assert (fd[:2] if fd else None) == (firsts[0] if firsts else None)
+        assert np.array_equal(rt.read_array(oa), data) or ovote.reference_first_divergence(rt.read_array(oa), data,
+                                                                                           1e-3) is None
+        assert ovote.reference_first_divergence(rt.read_array(ob), data + np.float32(1), 1e-3) is None
+    assert launches and all(c == 2 for c in launches)

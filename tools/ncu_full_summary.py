@@ -2,7 +2,8 @@
 .ncu-rep brought back from gpurun): duration, clock, DRAM bytes and %,
 pipe utilisation, occupancy, registers, grid, top warp-stall reasons.
 
-    python tools/ncu_full_summary.py gpurun_out/r02_full.ncu-rep "header line" ... > profiles/r02_ncu_full_summary.txt
+    python tools/ncu_full_summary.py [--all] gpurun_out/r02_full.ncu-rep "header line" ... > profiles/r02_ncu_full_summary.txt
+(--all: every captured launch, not the first of each kernel name)
 """
 import csv
 import io
@@ -28,7 +29,10 @@ METRICS = [
 ]
 STALL_PREFIX = "smsp__average_warp_latency_issue_stalled_"
 
-rep, *header = sys.argv[1:]
+args = sys.argv[1:]
+every = "--all" in args
+args = [a for a in args if a != "--all"]
+rep, *header = args
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units = rows[0], rows[1]
@@ -37,10 +41,10 @@ for h in header:
 seen = set()
 for r in rows[2:]:
     name = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "").strip()
-    if name in seen:
+    if name in seen and not every:
         continue
     seen.add(name)
-    print(f"\n== {name}")
+    print(f"\n== {name}" + (f"  (launch {r[hdr.index('ID')]})" if every and "ID" in hdr else ""))
     for label, m in METRICS:
         if m in hdr:
             i = hdr.index(m)
