@@ -841,6 +841,10 @@ def kernel_rooflines(device, n, kernels, torch):
         st.synchronize()
         return e0.elapsed_time(e1) * 1e-3 / iters
 
+    def vote_kernel_s(ws):
+        # the vote kernel's own clock (hf_vote_result.kernel_ns) of the last launch
+        return ws.read().kernel_ns * 1e-9
+
     m = n * n
     base = torch.rand(m, device=d) + 1
     reps = [base * (1 + 1e-6 * torch.randn(m, device=d)) for _ in range(3)]
@@ -849,9 +853,12 @@ def kernel_rooflines(device, n, kernels, torch):
     for K in (2, 3):
         t = time_it(lambda: kernels.vote_async(reps[:K], ws, 1e-3, voted=reps[0] if K >= 3 else None, stream=st))
         byts = K * m * 4      # replica reads; the in-place voted output stores only differing vectors
+        tk = vote_kernel_s(ws)
         out[f"hf_vote_K{K}"] = {"bound": "hbm", "achieved": byts / t / 1e9, "peak": peaks["hbm_gbs"],
                                 "unit": "GB/s", "frac": byts / t / 1e9 / peaks["hbm_gbs"],
                                 "us": t * 1e6, "algorithmic_bytes": byts,
+                                "kernel_us": tk * 1e6, "frac_kernel_clock": byts / tk / 1e9 / peaks["hbm_gbs"]
+                                if tk > 0 else None,
                                 "note": "voted output written in place over replica 0 (only differing "
                                         "vectors stored)" if K >= 3 else "no voted output (K = 2 verdict only)"}
     dst = torch.empty_like(base)

@@ -36,6 +36,62 @@ class VoterKernelProfile:
         return max(1, round(self.base_ns + self.per_byte_ns * size_bytes))
 
 
+class VoterCostModel:
+    """Learnt voter cost (new): a least-squares line ns = base + per_byte ·
+    bytes through the voter's own measured durations (hf_vote's kernel
+    clock), per (voter kernel, unit kind).  The executor feeds it every
+    measured vote; `apply` rewrites the matching VoterKernelProfile, so
+    place_voter (voting.py:146-174) ranks placements by measured cost instead
+    of constants.  Only kernels that report measured time are learnt (the
+    B200 "hf_vote" profiles); the reference's calibrated voter_single /
+    voter_parallel / voter_gpu constants of modelled fleets are untouched.
+    With a single distinct size the slope is the mean ns per byte and the
+    base keeps its prior."""
+
+    def __init__(self):
+        self._s: dict = {}
+
+    def observe(self, kernel: str, unit_kind: str, nbytes: int, ns: int) -> bool:
+        """Add one measurement; True when the fit should be re-applied (after
+        the 1st, 2nd, 4th, 8th, ... observation, then every 256th): placements
+        are cached between refits."""
+        if nbytes <= 0 or ns <= 0:
+            return False
+        n, sx, sy, sxx, sxy, xs = self._s.get((kernel, unit_kind), (0, 0.0, 0.0, 0.0, 0.0, frozenset()))
+        x, y = float(nbytes), float(ns)
+        new_size = nbytes not in xs and len(xs) < 4
+        if new_size:
+            xs = xs | {nbytes}
+        n += 1
+        self._s[(kernel, unit_kind)] = (n, sx + x, sy + y, sxx + x * x, sxy + x * y, xs)
+        return new_size or (n & (n - 1)) == 0 or n % 256 == 0
+
+    def fit(self, kernel: str, unit_kind: str):
+        """(base_ns, per_byte_ns) or None before the first observation."""
+        st = self._s.get((kernel, unit_kind))
+        if st is None:
+            return None
+        n, sx, sy, sxx, sxy, xs = st
+        if len(xs) >= 2:
+            den = n * sxx - sx * sx
+            if den > 0:
+                slope = (n * sxy - sx * sy) / den
+                base = (sy - slope * sx) / n
+                if slope > 0 and base >= 0:
+                    return base, slope
+        return None, sy / sx
+
+    def apply(self, profiles) -> None:
+        for prof in profiles:
+            f = self.fit(prof.kernel, prof.unit_kind)
+            if f is None:
+                continue
+            base, per = f
+            if base is not None:
+                prof.base_ns = int(round(base))
+            prof.per_byte_ns = per
+
+
 # hf_vote on a B200: ~10 us launch+sync floor, (K+1)·n bytes at ~6 TB/s; the
 # profile is per compared byte (K·n), so 1/6000 ns per byte is a lower bound
 B200_VOTER_BASE_NS = 10_000
@@ -62,6 +118,7 @@ class VoterConfig:
     profiles: list = field(default_factory=default_voter_profiles)
     kernel_delta: dict = field(default_factory=dict)   # per-variant δ (kernel -> δ)
     ulp_tolerance: Optional[int] = None                # float pairs also agree within N ulps
+    learn_costs: bool = True                           # measured votes refit the hf_vote profiles
 
     def __post_init__(self):
         if self.float_delta < 0:

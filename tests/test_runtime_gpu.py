@@ -528,3 +528,21 @@ def test_multi_area_task_votes_in_one_batch_launch():
                                                                                            1e-3) is None
         assert ovote.reference_first_divergence(rt.read_array(ob), data + np.float32(1), 1e-3) is None
     assert launches and all(c == 2 for c in launches)
+
+
+def test_voter_placement_costs_are_learnt_from_measured_votes():
+    """VoterConfig.learn_costs: every measured vote's kernel time refits the
+    hf_vote profiles place_voter ranks by (reference placement: voting.py:
+    146-174, calibrated constants voting.py:37-42).  After votes at two
+    sizes the fitted rate is the device's, not the prior constant."""
+    rt, task = matmul_runtime(kinds=("gpu-tc", "gpu-simt", "gpu-tc3"))
+    for n in (512, 1024, 512, 1024):
+        a, b = omatmul.make_inputs(n, seed=n)
+        _, _, _, args = register_mm(rt, a, b)
+        assert rt.invoke(task, args, hf.Strategy(hf.StrategyKind.HET_TMR)).success
+    profs = [p for p in rt.config.voter.profiles if p.kernel == "hf_vote" and p.unit_kind == "*"]
+    assert profs
+    per = profs[0].per_byte_ns
+    gbs = 1.0 / per           # bytes per ns = GB/s
+    assert 200 < gbs < 12_000, gbs
+    assert profs[0].base_ns >= 0

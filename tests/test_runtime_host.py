@@ -590,3 +590,26 @@ class TestCommitFidelity:
         got = np.frombuffer(rt.read_area(o), dtype=np.float32)
         want = ((DATA + np.float32(1.0)) * np.float32(1.0 + 2 ** -12)).astype(np.float32)
         assert got.tobytes() == want.tobytes()
+
+
+# ---- learnt voter cost (VoterCostModel) ---------------------------------------------
+
+def test_voter_cost_model_fits_measured_line():
+    m = hf.voting.VoterCostModel()
+    for nbytes in (1 << 20, 1 << 24, 1 << 26, 1 << 24):
+        m.observe("hf_vote", "gpu-simt", nbytes, round(2_000 + nbytes / 800))    # 800 B/ns = 0.8 TB/s
+    base, per = m.fit("hf_vote", "gpu-simt")
+    assert abs(base - 2_000) < 2 and abs(per * 800 - 1) < 1e-4
+    prof = hf.VoterKernelProfile("hf_vote", "gpu-simt", 10_000, 1.0)
+    m.apply([prof])
+    assert prof.base_ns == round(base) and prof.per_byte_ns == per
+
+
+def test_voter_cost_model_single_size_uses_mean_rate_and_keeps_base():
+    m = hf.voting.VoterCostModel()
+    assert m.observe("hf_vote", "*", 1000, 500)          # first observation: refit
+    assert m.fit("hf_vote", "*") == (None, 0.5)
+    prof = hf.VoterKernelProfile("hf_vote", "*", 7, 9.0)
+    m.apply([prof])
+    assert (prof.base_ns, prof.per_byte_ns) == (7, 0.5)
+    assert m.fit("hf_vote", "cpu") is None
