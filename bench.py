@@ -17,8 +17,10 @@ task.
   dmr    BASELINE configs[1] (HetDMR, TC vs SIMT, detect-and-rerun), extra key
 N > 1: one process per GPU, each running its own independent task stream
 (weak scaling, no data-path collective); timing is max over ranks.  With
-N >= 3, rank 0 also runs configs[2] ("c3": the three replicas on GPUs 0/1/2,
-the vote sliced over them reading peer replicas over NVLink).
+N >= 2, rank 0 also sweeps cross-GPU votes ("c4_cross_gpu": K replicas on K
+GPUs, the vote sliced over them, NVLink ingress per GPU against a measured
+P2P peak) and with N >= 3 runs configs[2] ("c3": the three replicas on GPUs
+0/1/2, inputs pulled over NVLink, the sliced vote).
 
 --impl reference times the reference's own CPU implementation of the same
 task on the host cores: hetrt from baseline/_ref (its MemoryManager with a
@@ -61,6 +63,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dmr", action="store_true", help="skip the HetDMR (configs[1]) side measurement")
     ap.add_argument("--no-c3", action="store_true", help="skip the replicas-on-3-GPUs sub-measurement (N >= 3)")
+    ap.add_argument("--c4-devices", default=None,
+                    help="run the cross-GPU vote sweep on these GPUs at any N (e.g. 0,0,0: one-GPU code-path check)")
     ap.add_argument("--c3-devices", default=None,
                     help="run the c3 sub-measurement on these GPUs at any N (e.g. 0,0,0: one-GPU code-path check)")
     ap.add_argument("--detect-probes", type=int, default=2000)
@@ -567,6 +571,12 @@ def run_hetft_arm(args, rank, world, local):
     # ---- kernel-level measurements (same process, after the timed regions) ----
     kern = kernel_rooflines(device, n, kernels, torch)
     detect = detect_rate(device, n, kernels, torch, args.seed, probes=args.detect_probes) if rank == 0 else None
+    c4x = None
+    if rank == 0 and not args.no_c3:
+        if world >= 2 and not shared_gpu and torch.cuda.device_count() >= 2:
+            c4x = c4_cross(args, torch, tuple(range(min(5, torch.cuda.device_count()))))
+        elif args.c4_devices:
+            c4x = c4_cross(args, torch, tuple(int(x) for x in args.c4_devices.split(",")))
     c3 = None
     if rank == 0 and not args.no_c3:
         if world >= 3 and not shared_gpu and torch.cuda.device_count() >= 3:
@@ -629,6 +639,7 @@ def run_hetft_arm(args, rank, world, local):
         "voter_gbs_in_task": vote_gbs,
         "dmr": dmr,
         "c3": c3,
+        "c4_cross_gpu": c4x,
         "detect": detect,
         "faults": {"injected": stats["injected"], "corrected_votes": stats["corrected"],
                    "mismatch_votes": stats["mismatch"], "votes": stats["votes"], "rounds": stats["rounds"]},
@@ -664,6 +675,51 @@ def p2p_peak(src_dev: int, dst_dev: int, torch, nbytes: int = 1 << 30):
                 t = e0.elapsed_time(e1) * 1e-3
                 best = t if best is None else min(best, t)
     return nbytes / best / 1e9
+
+
+def c4_cross(args, torch, devices):
+    """BASELINE configs[3] across GPUs: K replicas of 64 MiB / 256 MiB / 1 GiB
+    on `devices` (one per replica), voted sliced over them
+    (CudaBackend._vote_sliced_start: each GPU votes 1/K of the elements,
+    loading the other K-1 replicas' slices from their peers), K = 2..min(5,
+    GPUs).  Reports the vote time (max of the slices' own kernel clocks and
+    the CUDA events on the lead GPU) and each GPU's NVLink ingress rate,
+    (K-1)/K * n * 4 bytes / time, against the measured P2P peak."""
+    import paper_1405_2912_b200 as hf
+    from paper_1405_2912_b200.backend import CudaBackend
+    try:
+        be = CudaBackend()
+        peak = p2p_peak(devices[1], devices[0], torch) if len(set(devices)) > 1 else None
+        rows = []
+        for mib in (64, 256, 1024):
+            for K in range(2, min(5, len(devices)) + 1):
+                n = mib << 18
+                devs = devices[:K]
+                bufs = []
+                for d in devs:
+                    g = torch.Generator(device=f"cuda:{d}")
+                    g.manual_seed(17)
+                    bufs.append((torch.rand(n, device=f"cuda:{d}", generator=g) + 1).view(torch.uint8))
+                for d in set(devs):
+                    torch.cuda.synchronize(d)
+                ts = []
+                for it in range(6):
+                    h = be.vote_start(bufs, hf.ValueType.FLOAT32, 4, [1e-3] * K)
+                    res, ns = h.wait()
+                    assert res.verdict == "match"
+                    if it >= 2:
+                        ts.append(ns)
+                t = sorted(ts)[len(ts) // 2] * 1e-9
+                ingress = (K - 1) / K * n * 4
+                rows.append({"mib": mib, "K": K, "devices": list(devs), "vote_us": t * 1e6,
+                             "nvlink_ingress_gbs_per_gpu": ingress / t / 1e9 if len(set(devs)) > 1 else None,
+                             "frac_p2p_peak": (ingress / t / 1e9 / peak) if peak and len(set(devs)) > 1 else None,
+                             "replica_read_gbs": K * n * 4 / t / 1e9})
+                del bufs
+        return {"p2p_peak_gbs": peak, "peak_source": "measured: hf_copy 1 GiB peer pull (bench.p2p_peak)",
+                "rows": rows}
+    except Exception as exc:  # noqa: BLE001 - reported, the headline line still prints
+        return {"error": f"{type(exc).__name__}: {exc}"}
 
 
 def c3_rate(args, torch, devices=(0, 1, 2)):
