@@ -43,6 +43,21 @@ K.vote_bytes([x.view(torch.uint8)[: 12 * 1000] for x in ints], 12)
 ws = K.VoteWorkspace(0)
 K.vote_async([base, base.clone()], ws, 1e-3)
 ws.read()
+# round 2: K = 3 in place with the divergence in replica 0 (first-divergence
+# records + leader epilogue), and a batched launch of mixed sizes
+reps = [base.clone() for _ in range(3)]
+K.inject_bitflip(reps[0], 777, 30)
+K.inject_bitflip(reps[2], 70_000, 29)
+r3 = K.vote(reps, 1e-3, voted=reps[0])
+assert r3.first_div == 777 and r3.first_raw0 is not None
+items = []
+for m_ in (1, 17, 5000, 1 << 16, (1 << 18) + 5):
+    rr = [base[:m_].clone() for _ in range(3)]
+    K.inject_bitflip(rr[1], m_ // 2, 30)
+    items.append((rr, rr[0], K.VoteWorkspace(0), None))
+K.vote_batch(items, 1e-3)
+for it in items:
+    it[2].read()
 # copies, checkpoint + checksum, restore, fill, scribble, scale injection
 dst = torch.empty_like(base)
 cs = K.checkpoint(dst, base, with_checksum=True)
