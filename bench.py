@@ -574,7 +574,7 @@ def run_hetft_arm(args, rank, world, local):
     c4x = None
     if rank == 0 and not args.no_c3:
         if world >= 2 and not shared_gpu and torch.cuda.device_count() >= 2:
-            c4x = c4_cross(args, torch, tuple(range(min(5, torch.cuda.device_count()))))
+            c4x = c4_cross(args, torch, tuple(range(min(5, world, torch.cuda.device_count()))))
         elif args.c4_devices:
             c4x = c4_cross(args, torch, tuple(int(x) for x in args.c4_devices.split(",")))
     c3 = None
