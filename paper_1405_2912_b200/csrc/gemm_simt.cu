@@ -127,40 +127,39 @@ sgemm_128x128(const float* __restrict__ At, const float* __restrict__ B, float* 
     }
     // running total += chunk sum (acc pair (i, j) <-> Tot[q = 2i + j/2], half
     // j&1), then the chain restarts at zero.  Written in asm that updates
-    // the accumulators in place, behind a branch inside the asm, and called
-    // from the single k-tile loop: a C++ restart at zero (or a nested chunk
-    // loop) gave every accumulator a second definition, ptxas assigned them
-    // different registers and the loop back-edge grew ~32 MOVs per k-tile
-    // (+4.5% time).  `go` is warp-uniform.
+    // the accumulators in place, called behind a uniform branch from the
+    // single k-tile loop: a C++ restart at zero (or a nested chunk loop) gave
+    // every accumulator a second definition, ptxas assigned them different
+    // registers and the loop back-edge grew ~32 MOVs per k-tile (+4.5%
+    // time).  Of the loop shapes tried (tools/simt_ab.py,
+    // profiles/r02_simt_ab_fv.jsonl) this one is fastest: +3.7% over the
+    // single chain (branch inside the asm +4.2%, two k-tiles per test +5.8%,
+    // a countdown instead of the modulo +4.2%).
     const uint32_t tot_s = static_cast<uint32_t>(__cvta_generic_to_shared(Tot + t));
-    auto flush = [&](uint32_t go) {
+    auto flush = [&]() {
 #pragma unroll
         for (int i = 0; i < 8; i += 2)
             asm volatile(
-                "{\n\t.reg .pred p;\n\t.reg .b64 t0, t1, t2, t3, t4, t5, t6, t7;\n\t"
-                "setp.eq.u32 p, %8, 0;\n\t"
-                "@p bra.uni FLUSH_SKIP%=;\n\t"
-                "ld.shared.v2.b64 {t0, t1}, [%9];\n\t"
-                "ld.shared.v2.b64 {t2, t3}, [%9+4096];\n\t"
-                "ld.shared.v2.b64 {t4, t5}, [%9+8192];\n\t"
-                "ld.shared.v2.b64 {t6, t7}, [%9+12288];\n\t"
+                "{\n\t.reg .b64 t0, t1, t2, t3, t4, t5, t6, t7;\n\t"
+                "ld.shared.v2.b64 {t0, t1}, [%8];\n\t"
+                "ld.shared.v2.b64 {t2, t3}, [%8+4096];\n\t"
+                "ld.shared.v2.b64 {t4, t5}, [%8+8192];\n\t"
+                "ld.shared.v2.b64 {t6, t7}, [%8+12288];\n\t"
                 "add.rn.f32x2 t0, t0, %0;\n\tadd.rn.f32x2 t1, t1, %1;\n\t"
                 "add.rn.f32x2 t2, t2, %2;\n\tadd.rn.f32x2 t3, t3, %3;\n\t"
                 "add.rn.f32x2 t4, t4, %4;\n\tadd.rn.f32x2 t5, t5, %5;\n\t"
                 "add.rn.f32x2 t6, t6, %6;\n\tadd.rn.f32x2 t7, t7, %7;\n\t"
-                "st.shared.v2.b64 [%9], {t0, t1};\n\t"
-                "st.shared.v2.b64 [%9+4096], {t2, t3};\n\t"
-                "st.shared.v2.b64 [%9+8192], {t4, t5};\n\t"
-                "st.shared.v2.b64 [%9+12288], {t6, t7};\n\t"
+                "st.shared.v2.b64 [%8], {t0, t1};\n\t"
+                "st.shared.v2.b64 [%8+4096], {t2, t3};\n\t"
+                "st.shared.v2.b64 [%8+8192], {t4, t5};\n\t"
+                "st.shared.v2.b64 [%8+12288], {t6, t7};\n\t"
                 "mov.b64 %0, 0;\n\tmov.b64 %1, 0;\n\tmov.b64 %2, 0;\n\tmov.b64 %3, 0;\n\t"
-                "mov.b64 %4, 0;\n\tmov.b64 %5, 0;\n\tmov.b64 %6, 0;\n\tmov.b64 %7, 0;\n\t"
-                "FLUSH_SKIP%=:\n\t}"
+                "mov.b64 %4, 0;\n\tmov.b64 %5, 0;\n\tmov.b64 %6, 0;\n\tmov.b64 %7, 0;\n\t}"
                 : "+l"(acc[i][0]), "+l"(acc[i][1]), "+l"(acc[i][2]), "+l"(acc[i][3]),
                   "+l"(acc[i + 1][0]), "+l"(acc[i + 1][1]), "+l"(acc[i + 1][2]), "+l"(acc[i + 1][3])
-                : "r"(go), "r"(tot_s + static_cast<uint32_t>(2 * i * 256 * 16))
+                : "r"(tot_s + static_cast<uint32_t>(2 * i * 256 * 16))
                 : "memory");
     };
-
     const int nk = K / SB_K;
     pdl_wait();     // launched with PDL behind the A^T pre-pass: At is complete from here
 #pragma unroll
@@ -208,7 +207,9 @@ sgemm_128x128(const float* __restrict__ At, const float* __restrict__ B, float* 
     };
     for (int kt = 0; kt < nk; ++kt) {
         ktile(kt);
-        if constexpr (CH > 0) flush(static_cast<uint32_t>((kt + 1) % CH == 0 || kt + 1 == nk));
+        if constexpr (CH > 0) {
+            if ((kt + 1) % CH == 0 || kt + 1 == nk) flush();
+        }
     }
     cp_async_wait<0>();
     if constexpr (CH > 0) {

@@ -29,17 +29,13 @@ print(statistics.median(ts), min(ts), err)
 '''
 
 for n in [int(x) for x in sys.argv[1:]] or [4096, 2048]:
-    for v in ("r01", "chain", "32", "64", "r01", "chain", "32", "64"):
+    for v in ("chain", "blocked", "chain", "blocked"):
         env = dict(os.environ)
-        if v == "r01":        # round-1 library (built from git HEAD~ into tools/ab/, untracked)
-            env["HETFT_LIB"] = "tools/ab/libhetft_r01.so"
-        elif v.startswith("chain"):
+        if v.startswith("chain"):
             env["HF_SGEMM_CHAIN"] = "1"
             if v == "chain-smem112":      # chain kernel with the blocked kernel's smem footprint
                 env["HF_SGEMM_COSCHED_SMEM"] = "114688"
                 env["AB_MODE"] = str(0x100)
-        else:
-            env["HF_SGEMM_CH"] = v
         out = subprocess.run([sys.executable, "-c", CODE, str(n)], env=env, capture_output=True, text=True)
         med, mn, err = out.stdout.split() if out.returncode == 0 else ("nan", "nan", out.stderr[-300:])
         print(json.dumps({"n": n, "variant": v,
