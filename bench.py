@@ -355,7 +355,6 @@ class TaskStreamBench:
         gen.manual_seed(args.seed * 7919 + rank)
         self.A = (torch.rand(n * n, device=f"cuda:{device}", generator=gen) + 1).view(torch.uint8)
         self.B = (torch.rand(n * n, device=f"cuda:{device}", generator=gen) + 1).view(torch.uint8)
-        self.C0 = torch.zeros(self.nb, dtype=torch.uint8, device=f"cuda:{device}")
         self.strat = strategy if isinstance(strategy, hf.Strategy) else hf.Strategy(strategy)
         self.stream = self.rt.backend.stream(device)
         self.stats = {"tasks": 0, "rounds": 0, "votes": {}, "injected": 0, "mismatch": 0, "corrected": 0,
@@ -385,12 +384,17 @@ class TaskStreamBench:
         task i+1's replicas are queued on the GPU before task i's verdict is
         read, so host-side settling overlaps kernels."""
         rt, hf, n = self.rt, self.hf, self.n
+        hZ = self._host_buffers()[3]
         queue = []
         with rt.task_stream(depth=self.args.depth) as ts:
             for _ in range(steps):
                 ia = rt.register_device_data(self.A, n * n, hf.ValueType.FLOAT32, "r", self.space)
                 ib = rt.register_device_data(self.B, n * n, hf.ValueType.FLOAT32, "r", self.space)
-                ic = rt.register_device_data(self.C0, n * n, hf.ValueType.FLOAT32, "w", self.space)
+                # the output area as reference programs register it (a host
+                # payload of zeros; the reference arm does the same): a "w"
+                # request never reads it, and with a host copy it is not a
+                # sole device copy, so no checkpoint of C
+                ic = rt.register_host_buffer(hZ, n * n, hf.ValueType.FLOAT32, "w")
                 queue.append((ts.submit(self.task, {"A": ia, "B": ib, "C": ic, "n": n}, self.strat), (ia, ib, ic)))
                 while queue and queue[0][0].success:
                     rep, areas = queue.pop(0)

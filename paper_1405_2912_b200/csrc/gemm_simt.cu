@@ -387,6 +387,9 @@ extern "C" int hf_gemm_simt(const float* A, const float* B, float* C, int M, int
             // replica's pre-pass, so the SIMT grid is pending first)
             hf::SideStream* side = (mode & HF_GEMM_COSCHEDULE) ? hf::side_stream(device, 0) : nullptr;
             cudaStream_t ps = st;
+            // (r2: the GEMM on the side stream right behind the pre-pass, plain
+            // or PDL, removes the event gap but lost 1.6% per HetTMR task and
+            // 0-1.6% per HetDMR task: 345 vs 350.5 tasks/s, tools/tmr_order_ab.py)
             HF_CUDA_CHECK(hf::begin_side_launch(side, st, &ps));
             hf::transpose_a<<<dim3(K / 32, M / 32), 256, 0, ps>>>(A, At, M, K);
             HF_CUDA_CHECK(hf::end_side_launch(side, st));

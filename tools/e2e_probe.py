@@ -42,7 +42,7 @@ if args.tmr:
                                                          attempt_limit=64))
     task = hf.get_workload("matmul").attach(rt, kinds=kinds)
 else:
-    hf, rt, task = bench.build_runtime(0, args.p, 1)
+    hf, rt, task = bench.build_runtime(0, args.p, 1, kinds=bench.DMR_KINDS)
 n = args.n
 nb = n * n * 4
 space = "gpu0mem"

@@ -19,6 +19,7 @@ from paper_1405_2912_b200 import executor as ex  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--steps", type=int, default=40)
 ap.add_argument("--variants", default="default,tc3-first")
+ap.add_argument("--dmr", action="store_true", help="HetDMR (TC + SIMT) instead of HetTMR")
 a = ap.parse_args()
 args = argparse.Namespace(n=4096, fault_prob=0.05, seed=1, depth=1, warmup=3, trace_steps=False)
 
@@ -28,7 +29,8 @@ orig = ex.Executor._expected_ns
 for name in a.variants.split(",") * 2:
     r = RANK[name]
     ex.Executor._expected_ns = orig if r is None else (lambda self, task, sel, r=r: float(r[sel.kernel]))
-    b = bench.TaskStreamBench(args, 0, 0, bench.TMR_KINDS, hf.StrategyKind.HET_TMR)
+    b = bench.TaskStreamBench(args, 0, 0, bench.DMR_KINDS if a.dmr else bench.TMR_KINDS,
+                              hf.StrategyKind.HET_DMR if a.dmr else hf.StrategyKind.HET_TMR)
     b.warm()
     t, _ = b.timed(b.device_stream, a.steps, True)
     print(json.dumps({"variant": name, "tasks_per_s": a.steps / t, "ms_per_task": 1e3 * t / a.steps,
