@@ -935,8 +935,11 @@ def kernel_rooflines(device, n, kernels, torch):
                          "unit": "TFLOP/s", "frac": 2 * n ** 3 / t / 1e12 / tf32_peak, "us": t * 1e6,
                          "peak_source": "measured bf16 dense / 2 (tf32 rate)", "includes": "B^T + RN pre-pass"}
     t = time_it(lambda: kernels.gemm_simt(a, b, c, stream=st), iters=5)
+    ffma_peak, _src = fp32_peak(1965.0)
     out["hf_gemm_simt"] = {"bound": "fp32-simt", "achieved": 2 * n ** 3 / t / 1e12, "unit": "TFLOP/s",
-                           "us": t * 1e6}
+                           "peak": ffma_peak, "frac": 2 * n ** 3 / t / 1e12 / ffma_peak, "us": t * 1e6,
+                           "note": "standalone (alone on the GPU, incl. the A^T pre-pass); the headline "
+                                   "roofline is the same kernel in-task, sharing SMs with two TC replicas"}
     return out
 
 
