@@ -792,7 +792,18 @@ def c3_rate(args, torch, devices=(0, 1, 2)):
         return {"error": f"{type(exc).__name__}: {exc}"}
 
 
+_FP32_PEAK = None
+
+
 def fp32_peak(sm_max_mhz: float):
+    """Cached: the probe runs once per bench process."""
+    global _FP32_PEAK
+    if _FP32_PEAK is None:
+        _FP32_PEAK = _fp32_peak(sm_max_mhz)
+    return _FP32_PEAK
+
+
+def _fp32_peak(sm_max_mhz: float):
     """FP32 SIMT peak for the SIMT variant's roofline (MEASURED_PEAKS.json has
     none): the packed-FFMA2 probe tools/fp32_peak (built by build()) run live
     on this GPU, else the round's committed probe result, else nominal."""
