@@ -47,3 +47,38 @@ def test_no_device_reports_cleanly():
     rc = lib.hf_init(0, 1)
     assert rc == _lib.HF_ENOINIT
     assert "no CUDA device" in _lib.last_error()
+
+
+def test_struct_layouts_match_the_c_header(tmp_path):
+    """Compile a probe against include/hetft.h with the host C compiler and
+    compare sizeof/offsetof of hf_vote_result and hf_vote_item (and
+    HF_VOTE_BATCH_MAX) with the ctypes mirrors in _lib."""
+    import shutil
+    import subprocess
+    from pathlib import Path
+    from paper_1405_2912_b200 import _lib
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    inc = Path(__file__).resolve().parents[1] / "include"
+    src = tmp_path / "probe.c"
+    fields_r = [f for f, _ in _lib.HfVoteResult._fields_]
+    fields_i = [f for f, _ in _lib.HfVoteItem._fields_]
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "hetft.h"', "int main(void) {",
+             'printf("R %zu\\n", sizeof(hf_vote_result));', 'printf("I %zu\\n", sizeof(hf_vote_item));',
+             'printf("B %d\\n", HF_VOTE_BATCH_MAX);']
+    lines += [f'printf("r.{f} %zu\\n", offsetof(hf_vote_result, {f}));' for f in fields_r]
+    lines += [f'printf("i.{f} %zu\\n", offsetof(hf_vote_item, {f}));' for f in fields_i]
+    lines += ["return 0; }"]
+    src.write_text("\n".join(lines) + "\n")
+    exe = tmp_path / "probe"
+    subprocess.run([cc, "-I", str(inc), str(src), "-o", str(exe)], check=True)
+    got = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                        check=True).stdout.splitlines())
+    assert int(got["R"]) == ctypes.sizeof(_lib.HfVoteResult)
+    assert int(got["I"]) == ctypes.sizeof(_lib.HfVoteItem)
+    assert int(got["B"]) == _lib.HF_VOTE_BATCH_MAX
+    for f in fields_r:
+        assert int(got[f"r.{f}"]) == getattr(_lib.HfVoteResult, f).offset, f
+    for f in fields_i:
+        assert int(got[f"i.{f}"]) == getattr(_lib.HfVoteItem, f).offset, f
