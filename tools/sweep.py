@@ -54,10 +54,15 @@ def main(out=Path("gpurun_out/sweep.json"), sizes=None, diverse=False):
             ws = kernels.VoteWorkspace(0, stream=st)
             voted = reps[0] if K >= 3 else None
             t = timed(lambda: kernels.vote_async(reps, ws, 1e-3, voted=voted, stream=st), st, iters)
+            tk = ws.read().kernel_ns * 1e-9          # the last launch's own clock (r2)
             rd = K * nbytes
             rows.append({"kernel": "hf_vote", "K": K, "diverse": diverse, "bytes_per_replica": nbytes, "us": t * 1e6,
                          "read_GBps": rd / t / 1e9, "frac_of_hbm": rd / t / 1e9 / hbm,
+                         "kernel_us": tk * 1e6, "frac_of_hbm_kernel_clock": rd / tk / 1e9 / hbm if tk else None,
                          "survey_GBps_(K+1)n": (K + 1) * nbytes / t / 1e9})
+            # batched small votes: tools/vote_batch_sweep.py (distinct replica
+            # sets per vote; reusing these replicas 32 times would read them
+            # from the L2 and overstate the rate)
             print(json.dumps(rows[-1]), flush=True)
             del reps
         dst = torch.empty_like(base)
