@@ -613,3 +613,25 @@ def test_voter_cost_model_single_size_uses_mean_rate_and_keeps_base():
     m.apply([prof])
     assert (prof.base_ns, prof.per_byte_ns) == (7, 0.5)
     assert m.fit("hf_vote", "cpu") is None
+
+
+def test_nvtx_ranges_are_noops_unless_enabled():
+    from paper_1405_2912_b200 import nvtx
+    assert nvtx.ENABLED is False            # HETFT_NVTX unset in the test environment
+    with nvtx.range("x"):
+        pass
+
+
+def test_nvtx_enabled_pushes_and_pops(monkeypatch):
+    from paper_1405_2912_b200 import nvtx
+    calls = []
+    monkeypatch.setattr(nvtx, "ENABLED", True)
+    monkeypatch.setattr(nvtx, "_push", lambda name: calls.append(("push", name)))
+    monkeypatch.setattr(nvtx, "_pop", lambda: calls.append(("pop",)))
+    rt, task = runtime(three_units())
+    _, _, a = args_for(rt)
+    assert rt.invoke(task, a, DMR).success
+    names = [c[1] for c in calls if c[0] == "push"]
+    assert calls.count(("pop",)) == len(names)
+    assert any(n.startswith("hetft.vote") for n in names) and any(n.startswith("hetft.replica") for n in names)
+    assert any(n.startswith("hetft.settle") for n in names) and any(n.startswith("hetft.advance") for n in names)
