@@ -66,13 +66,19 @@ void preload_kernels(int device);
 struct DeviceGuard {
     int prev = -1;
     bool ok = true;
+    bool switched = false;
     explicit DeviceGuard(int dev) {
         if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
-        if (dev >= 0 && dev != prev) ok = cudaSetDevice(dev) == cudaSuccess;
+        if (dev >= 0 && dev != prev) {
+            ok = cudaSetDevice(dev) == cudaSuccess;
+            switched = ok;
+        }
         if (ok) preload_kernels(dev >= 0 ? dev : (prev >= 0 ? prev : 0));
     }
     ~DeviceGuard() {
-        if (prev >= 0) cudaSetDevice(prev);
+        // restore only what was changed: every C-ABI call takes a guard, and
+        // the common case (already on the right device) then costs one query
+        if (switched && prev >= 0) cudaSetDevice(prev);
     }
 };
 

@@ -98,7 +98,7 @@ def main():
         pairs.append((torch.from_numpy(a).view(-1).view(torch.uint8).to(d),
                       torch.from_numpy(b).view(-1).view(torch.uint8).to(d)))
         refs.append(torch.from_numpy(c).view(-1).to(d))
-    c0 = torch.zeros(nn * 4, dtype=torch.uint8, device=d)
+    hz = torch.zeros(nn * 4, dtype=torch.uint8).pin_memory()
     mine = sharding.tasks_for_rank(args.tasks, rank, world)
 
     cnt = {"tasks": 0, "rounds": 0, "attempts": 0, "injected_bitflips": 0, "aborts": 0, "api_errors": 0,
@@ -148,7 +148,10 @@ def main():
                 j = t % args.inputs
                 ia = rt.register_device_data(pairs[j][0], nn, hf.ValueType.FLOAT32, "r", space)
                 ib = rt.register_device_data(pairs[j][1], nn, hf.ValueType.FLOAT32, "r", space)
-                ic = rt.register_device_data(c0, nn, hf.ValueType.FLOAT32, "w", space)
+                # the output area as reference programs register it (host zeros,
+                # never read by a "w" request; not a sole device copy, so no
+                # checkpoint of C) — as bench.py does
+                ic = rt.register_host_buffer(hz, nn, hf.ValueType.FLOAT32, "w")
                 queue.append((ts.submit(task, {"A": ia, "B": ib, "C": ic, "n": n}, strat), j, (ia, ib, ic)))
                 while queue and queue[0][0].success:
                     rep, jj, areas = queue.pop(0)
