@@ -572,25 +572,29 @@ def run_hetft_arm(args, rank, world, local):
                if dmr_b.stats["vote_ns"] else None}
         del dmr_b
 
-    # ---- kernel-level measurements (same process, after the timed regions) ----
+    # ---- kernel-level measurements (rank 0, after the timed regions) ----
+    # the other ranks stop here: C3/C4 below drive GPUs 1.. from rank 0, so
+    # every rank's own work on its GPU must have drained first
+    total_tasks = args.steps * world
+    torch.cuda.synchronize()
+    barrier()
+    if rank != 0:
+        return
     kern = kernel_rooflines(device, n, kernels, torch)
-    detect = detect_rate(device, n, kernels, torch, args.seed, probes=args.detect_probes) if rank == 0 else None
+    detect = detect_rate(device, n, kernels, torch, args.seed, probes=args.detect_probes)
     c4x = None
-    if rank == 0 and not args.no_c3:
+    if not args.no_c3:
         if world >= 2 and not shared_gpu and torch.cuda.device_count() >= 2:
             c4x = c4_cross(args, torch, tuple(range(min(5, world, torch.cuda.device_count()))))
         elif args.c4_devices:
             c4x = c4_cross(args, torch, tuple(int(x) for x in args.c4_devices.split(",")))
     c3 = None
-    if rank == 0 and not args.no_c3:
+    if not args.no_c3:
         if world >= 3 and not shared_gpu and torch.cuda.device_count() >= 3:
             c3 = c3_rate(args, torch, devices=(0, 1, 2))
         elif args.c3_devices:       # code-path check, e.g. 0,0,0 on a one-GPU box
             c3 = c3_rate(args, torch, devices=tuple(int(x) for x in args.c3_devices.split(",")))
 
-    total_tasks = args.steps * world
-    if rank != 0:
-        return
     peaks, peak_src = load_peaks()
     stats = tmr.stats
     simt_ms, tc_ms, tc3_ms = tmr.kernel_ms("mm_simt"), tmr.kernel_ms("mm_tc"), tmr.kernel_ms("mm_tc3x")

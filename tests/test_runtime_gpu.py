@@ -536,7 +536,10 @@ def test_voter_placement_costs_are_learnt_from_measured_votes():
     146-174, calibrated constants voting.py:37-42).  After votes at two
     sizes the fitted rate is the device's, not the prior constant."""
     rt, task = matmul_runtime(kinds=("gpu-tc", "gpu-simt", "gpu-tc3"))
-    for n in (512, 1024, 512, 1024):
+    # sizes where the votes' kernel time is bandwidth- rather than
+    # latency-dominated (K = 3 reads of 12 and 48 MiB): at 1-4 MiB the slope
+    # between two sizes is noise on a few-microsecond fixed cost
+    for n in (1024, 2048, 1024, 2048):
         a, b = omatmul.make_inputs(n, seed=n)
         _, _, _, args = register_mm(rt, a, b)
         assert rt.invoke(task, args, hf.Strategy(hf.StrategyKind.HET_TMR)).success
@@ -544,5 +547,5 @@ def test_voter_placement_costs_are_learnt_from_measured_votes():
     assert profs
     per = profs[0].per_byte_ns
     gbs = 1.0 / per           # bytes per ns = GB/s
-    assert 200 < gbs < 12_000, gbs
+    assert 200 < gbs < 20_000, gbs     # 12 MiB reads can be partly L2-resident
     assert profs[0].base_ns >= 0
