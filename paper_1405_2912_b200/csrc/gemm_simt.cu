@@ -354,6 +354,14 @@ extern "C" int hf_gemm_simt(const float* A, const float* B, float* C, int M, int
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, hf::SGEMM_SMEM_MAX));
             HF_CUDA_CHECK(cudaFuncSetAttribute(hf::sgemm_128x128<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                hf::SGEMM_SMEM_MAX));
+            // the whole unified L1 as shared memory (the ring is filled by
+            // cp.async.cg, which bypasses L1): an SM running one SIMT CTA then
+            // still has room for a co-scheduled TC CTA beside it
+            HF_CUDA_CHECK(cudaFuncSetAttribute(hf::sgemm_128x128<hf::SGEMM_CH>,
+                                               cudaFuncAttributePreferredSharedMemoryCarveout,
+                                               cudaSharedmemCarveoutMaxShared));
+            HF_CUDA_CHECK(cudaFuncSetAttribute(hf::sgemm_128x128<0>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                               cudaSharedmemCarveoutMaxShared));
             attr[device] = true;
         }
         // HF_SGEMM_CHAIN=1 (A/B only): one fp32 chain over all of K, 48 KB

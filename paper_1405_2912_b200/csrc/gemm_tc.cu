@@ -884,6 +884,19 @@ static int cosched_bn() {
     return v;
 }
 
+// Co-scheduled grid cap (HF_TC_COSCHED_GRID, experiments only; default 0 =
+// one CTA per tile): the kernel is persistent, so a cap makes it hold that
+// many CTA slots for its whole run.
+static int cosched_grid() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("HF_TC_COSCHED_GRID");
+        v = e ? atoi(e) : 0;
+        if (v < 0) v = 0;
+    }
+    return v;
+}
+
 // Launch shape: CTA pairs (6 stages, double-buffered TMEM, 74 persistent
 // pairs) by default; single-CTA persistent (4 stages, grid = SMs) with
 // HF_GEMM_TC_PAIR=0 or below 256 x 256; co-scheduling (2 stages, 1
@@ -987,6 +1000,13 @@ static int launch(const void* A, const void* Bt, float* C, int M, int N, int K, 
                                            smem_bytes<2>()));
         HF_CUDA_CHECK(cudaFuncSetAttribute(gemm_tf32_kernel<3, 1, BF16, 128>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<3, 128>()));
+        // co-scheduled shapes share SMs with SIMT CTAs: whichever kernel's CTA
+        // reaches an idle SM first, the SM is configured all-shared
+        HF_CUDA_CHECK(cudaFuncSetAttribute(gemm_tf32_kernel<2, 1, BF16>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                           cudaSharedmemCarveoutMaxShared));
+        HF_CUDA_CHECK(cudaFuncSetAttribute(gemm_tf32_kernel<3, 1, BF16, 128>,
+                                           cudaFuncAttributePreferredSharedMemoryCarveout,
+                                           cudaSharedmemCarveoutMaxShared));
         attr_set[device] = true;
     }
     if (narrow) {
@@ -997,7 +1017,9 @@ static int launch(const void* A, const void* Bt, float* C, int M, int N, int K, 
         gemm_tf32_kernel<3, 1, BF16, 128><<<tiles_narrow, NUM_THREADS, smem_bytes<3, 128>(), st>>>(ta, tb, C, M, N,
                                                                                                 K);
     } else if (cosched) {
-        gemm_tf32_kernel<2, 1, BF16><<<tiles, NUM_THREADS, smem_bytes<2>(), st>>>(ta, tb, C, M, N, K);
+        const int cap = cosched_grid();
+        gemm_tf32_kernel<2, 1, BF16><<<cap > 0 && cap < tiles ? cap : tiles, NUM_THREADS, smem_bytes<2>(), st>>>(
+            ta, tb, C, M, N, K);
     } else {
         const int sms = num_sms(device);
         const int grid = tiles < sms ? tiles : sms;
