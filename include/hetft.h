@@ -122,7 +122,9 @@ int hf_vote(const void* const* replicas, int K, int64_t n, int dtype,
  * straight over the bus and no separate read-back copy is needed.  `workspace` is caller-owned device memory
  * of hf_vote_workspace_bytes() bytes initialised once with
  * hf_vote_workspace_init(); the kernel leaves it re-initialised, so one
- * workspace serves any number of back-to-back votes on one stream. */
+ * workspace serves any number of back-to-back votes on one stream.
+ * n = 0 is legal here and in hf_vote_batch items (one block writes a match
+ * result with first_div = -1, as the reference compares empty payloads). */
 int64_t hf_vote_workspace_bytes(void);
 int hf_vote_workspace_init(void* workspace, int device, void* stream);
 int hf_vote_async(const void* const* replicas, int K, int64_t n, int dtype,

@@ -951,7 +951,7 @@ static int launch_vote_batch(const hf_vote_item* items, int count, int K, int dt
     for (int i = 0; i < count; ++i) {
         HF_REQUIRE(items[i].out != nullptr && items[i].workspace != nullptr,
                    "hf_vote_batch: item %d has a NULL result/workspace", i);
-        HF_REQUIRE(items[i].n > 0, "hf_vote_batch: item %d has n <= 0", i);
+        HF_REQUIRE(items[i].n >= 0, "hf_vote_batch: item %d has n < 0", i);
         VoteParams p;
         int rc = fill_params(p, items[i].replicas, K, items[i].n, width, rel_tol, ulp_tol, items[i].voted);
         if (rc) return rc;
@@ -971,7 +971,8 @@ static int launch_vote_batch(const hf_vote_item* items, int count, int K, int dt
     int b = 0;
     for (int i = 0; i < count; ++i) {
         long long want = (work[i] + threads - 1) / threads;
-        long long share = static_cast<long long>(static_cast<double>(cap) * work[i] / total);
+        // an empty item still gets one block: it writes the item's result
+        long long share = total > 0 ? static_cast<long long>(static_cast<double>(cap) * work[i] / total) : 1;
         long long nb = want < share ? want : share;
         if (nb < 1) nb = 1;
         if (nb > kMaxVoteBlocks) nb = kMaxVoteBlocks;
@@ -1114,7 +1115,7 @@ int hf_vote_async(const void* const* replicas, int K, int64_t n, int dtype, cons
                   int device, void* stream) {
     HF_REQUIRE(hf::elem_size(dtype) > 0, "hf_vote_async: unknown dtype %d", dtype);
     HF_REQUIRE(dev_out != nullptr && workspace != nullptr, "hf_vote_async: NULL result/workspace");
-    HF_REQUIRE(n > 0, "hf_vote_async: n must be > 0");
+    HF_REQUIRE(n >= 0, "hf_vote_async: n must be >= 0");   // n = 0: one block writes a match result
     hf::VoteParams p;
     int rc = hf::fill_params(p, replicas, K, n, hf::elem_size(dtype), rel_tol, ulp_tol, voted);
     if (rc) return rc;

@@ -573,3 +573,37 @@ def test_vote_batch_rejects_mixed_items(K):
     b = [torch.rand(100, device="cuda") for _ in range(2)]
     with pytest.raises(ValueError):
         K.vote_batch([(a, None, ws, None), (b, None, ws, None)])
+
+
+@pytest.mark.parametrize("Kr", [2, 3])
+def test_empty_votes_async_and_batched(K, Kr):
+    """Empty replicas (the reference compares empty payloads as a match,
+    voting.py:68-81, and never corrupts them, devices.py:207-212): the
+    asynchronous and batched votes accept n = 0 and return match, no
+    mismatches, first divergence -1; a batch mixing empty and non-empty items
+    still votes the others exactly."""
+    import ctypes
+    from paper_1405_2912_b200 import _lib
+    e = [torch.empty(0, device="cuda") for _ in range(Kr)]
+    ws = K.VoteWorkspace(0)
+    out = torch.zeros(ctypes.sizeof(_lib.HfVoteResult), dtype=torch.uint8).pin_memory()
+    K.vote_async(e, ws, 1e-3, result_into=out)
+    torch.cuda.synchronize()
+    r = K.VoteResult.from_c(_lib.HfVoteResult.from_buffer_copy(out.numpy().tobytes()))
+    assert (r.verdict, r.mismatch, r.unresolved, r.first_div) == ("match", [0] * Kr, 0, -1)
+    rng = np.random.default_rng(Kr)
+    base = rng.uniform(1, 2, 3001).astype(np.float32)
+    reps = [base.copy() for _ in range(Kr)]
+    reps[1][1234] *= 2
+    items = []
+    for reps_i in ([np.empty(0, np.float32)] * Kr, reps, [np.empty(0, np.float32)] * Kr):
+        items.append(([dev(x) for x in reps_i], None, K.VoteWorkspace(0),
+                      torch.zeros(ctypes.sizeof(_lib.HfVoteResult), dtype=torch.uint8).pin_memory()))
+    K.vote_batch(items, 1e-3)
+    torch.cuda.synchronize()
+    got = [K.VoteResult.from_c(_lib.HfVoteResult.from_buffer_copy(it[3].numpy().tobytes())) for it in items]
+    for g in (got[0], got[2]):
+        assert (g.verdict, g.mismatch, g.unresolved, g.first_div) == ("match", [0] * Kr, 0, -1)
+    o = ovote.vote(reps, 1e-3)
+    assert (got[1].verdict, got[1].mismatch, got[1].unresolved, got[1].first_div) == \
+        (o.verdict, o.mismatch, o.unresolved, o.first_div)

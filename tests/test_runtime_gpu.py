@@ -549,3 +549,17 @@ def test_voter_placement_costs_are_learnt_from_measured_votes():
     gbs = 1.0 / per           # bytes per ns = GB/s
     assert 200 < gbs < 20_000, gbs     # 12 MiB reads can be partly L2-resident
     assert profs[0].base_ns >= 0
+
+
+
+def test_empty_areas_are_rejected_at_registration():
+    """The reference refuses zero-element areas (memory.py:92-93), so no task
+    ever votes an empty output; the drop-in raises the same error for host
+    and device-resident registrations (empty payloads still vote as a match
+    at the kernel level, test_kernels_gpu.py::test_empty_votes_async_and_batched)."""
+    rt, _task = matmul_runtime()
+    with pytest.raises(hf.RegistrationError):
+        rt.register_data(b"", 0, hf.ValueType.FLOAT32, "r")
+    with pytest.raises(hf.RegistrationError):
+        rt.register_device_data(torch.empty(0, dtype=torch.uint8, device="cuda"), 0, hf.ValueType.FLOAT32, "r",
+                                "gpu0mem")

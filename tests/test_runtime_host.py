@@ -247,6 +247,20 @@ def mm():
     return hf.MemoryManager(hf.load_fleet(three_units()), HostBackend())
 
 
+def test_register_buffer_checks_like_register(mm):
+    """Zero-copy registration (register_host_buffer / register_device_data)
+    applies register()'s checks (reference memory.py:88-101): no empty
+    areas, known value type and mode, a buffer large enough for the
+    elements."""
+    from host_backend import _HostBytes
+    buf = _HostBytes(16)
+    assert mm.register_buffer(buf, 4, hf.ValueType.FLOAT32, "r")
+    for args in ((0, hf.ValueType.FLOAT32, "r"), (5, hf.ValueType.FLOAT32, "r"), (4, "float32", "r"),
+                 (4, hf.ValueType.FLOAT32, "x"), (17, hf.ValueType.INT, "r")):
+        with pytest.raises(hf.RegistrationError):
+            mm.register_buffer(buf, *args)
+
+
 def floats(n, start=0.0):
     return np.arange(start, start + n, dtype=np.float32).tobytes()
 
