@@ -58,6 +58,15 @@ for m_ in (1, 17, 5000, 1 << 16, (1 << 18) + 5):
 K.vote_batch(items, 1e-3)
 for it in items:
     it[2].read()
+# empty votes (r2): async n = 0, and a batch mixing empty and non-empty items
+empty = [torch.empty(0, device=d) for _ in range(3)]
+ws_e = K.VoteWorkspace(0)
+K.vote_async(empty, ws_e, 1e-3)
+assert ws_e.read().verdict == "match"
+items = [(empty, None, K.VoteWorkspace(0), None), ([base[:999].clone() for _ in range(3)], None, K.VoteWorkspace(0), None),
+         (empty, None, K.VoteWorkspace(0), None)]
+K.vote_batch(items, 1e-3)
+assert all(it[2].read().verdict == "match" for it in items)
 # copies, checkpoint + checksum, restore, fill, scribble, scale injection
 dst = torch.empty_like(base)
 cs = K.checkpoint(dst, base, with_checksum=True)
