@@ -16,6 +16,7 @@ nothing under the package imports or falls back to it.
 
 from __future__ import annotations
 
+import os
 import threading
 from typing import Optional, Sequence
 
@@ -37,6 +38,12 @@ def torch_dtype(np_dtype) -> torch.dtype:
 
 
 _VIEW_DTYPES: dict = {}     # (ValueType, width) -> (numpy dtype, torch dtype) of typed_view
+
+# Votes run on their own per-device stream (r2; HETFT_VOTE_STREAM=0 puts them
+# back on the compute stream).  Priority: above the lead replica's stream, so
+# a finished task's vote is dispatched ahead of the next task's SIMT CTAs.
+VOTE_PRIORITY = -2
+_VOTE_STREAM = os.environ.get("HETFT_VOTE_STREAM", "1") != "0"
 
 
 class CudaBackend:
@@ -103,6 +110,39 @@ class CudaBackend:
         """The device's compute stream waits for `stream` (a unit stream)."""
         if stream is not None and device is not None:
             self.stream(device).wait_stream(stream)
+
+    def vote_stream(self, device: Optional[int]):
+        """The device's vote stream (r2).  A vote waits for its replicas'
+        streams (vote_after) and for the compute-stream work queued before it
+        (_vstream), but the compute stream never waits for a vote: the next
+        task's checkpoints, fills and replicas queue behind nothing of this
+        task's tensor-core tail.  Readers of a voted area wait on the vote's
+        event instead (Sibling.ready, MemoryManager._await); buffers a vote
+        read are dropped only after the host has seen its result."""
+        if device is None:
+            return None
+        if not _VOTE_STREAM:
+            return self.stream(device)
+        key = ("vote", device)
+        with self._lock:
+            s = self._streams.get(key)
+            if s is None:
+                s = torch.cuda.Stream(device=device, priority=VOTE_PRIORITY)
+                self._streams[key] = s
+        return s
+
+    def vote_after(self, stream, device: Optional[int]) -> None:
+        """The device's vote stream waits for `stream` (a replica's unit stream)."""
+        if stream is not None and device is not None:
+            self.vote_stream(device).wait_stream(stream)
+
+    def _vstream(self, device: int):
+        """The vote stream, ordered after everything queued on the device's
+        compute stream so far (callers outside the executor produce there)."""
+        vs = self.vote_stream(device)
+        if vs is not self.stream(device):
+            vs.wait_stream(self.stream(device))
+        return vs
 
     def copy_stream(self, device: int, direction: str = "h2d"):
         """Extra streams per device for host<->device traffic, one per
@@ -365,10 +405,10 @@ class CudaBackend:
             return DoneVote(*self.vote(bufs, value_type, width, rel_tol, ulp_tol, voted, device))
         if device is None:
             device = devs[0]
-        st = self.stream(device)
+        st = self._vstream(device)
         for d in devs:
             if d != device:
-                st.wait_stream(self.stream(d))
+                st.wait_stream(self._vstream(d))
         slot = self._vote_slot(device)
         start = self.timer_start(st, device)
         dt = torch_dtype(view_dtype(value_type, width))
@@ -393,7 +433,7 @@ class CudaBackend:
         slots and combine exactly in _PendingSliced.wait (counts add, first
         divergence = min)."""
         from .sharding import slice_bounds
-        streams = {d: self.stream(d) for d in devs}
+        streams = {d: self._vstream(d) for d in devs}
         # every slice reads every replica: each voting GPU waits for all producers
         evs = {d: self.record(streams[d]) for d in devs}
         for d in devs:
@@ -443,7 +483,7 @@ class CudaBackend:
         if len(devs) != 1 or len(dts) != 1:
             return single()
         dev = devs.pop()
-        st = self.stream(dev)
+        st = self._vstream(dev)
         dt = torch_dtype(dts.pop()[0])
         slots = [self._vote_slot(dev) for _ in specs]
         items = [([b.view(dt) for b in bufs], v.view(dt) if v is not None else None, slot.ws, slot.host)
@@ -462,6 +502,7 @@ class CudaBackend:
         gets to look at it."""
         for d in sorted({d for d in devices if d is not None}):
             self.stream(d)
+            self.vote_stream(d)
             slots = [self._vote_slot(d) for _ in range(vote_slots)]
             for sl in slots:
                 self._release_vote_slot(d, sl)
@@ -492,7 +533,7 @@ class CudaBackend:
         if self.slice_across_gpus and len(devs) >= 2 and typed:
             # replicas on distinct GPUs: every replica GPU votes its slice,
             # each waiting for all replica producers (cross-device events)
-            streams = {d: self.stream(d) for d in devs}
+            streams = {d: self._vstream(d) for d in devs}
             for d in devs:
                 for e in devs:
                     if e != d:
@@ -508,10 +549,10 @@ class CudaBackend:
             self.launches += len(devs)
             ns = stop()
             return res, (res.kernel_ns or ns)
-        st = self.stream(device)
+        st = self._vstream(device)
         for d in devs:
             if d != device:
-                st.wait_stream(self.stream(d))
+                st.wait_stream(self._vstream(d))
         start = self.timer_start(st, device)
         if value_type.numpy_dtype is None and width not in INT_DTYPES:
             res = kernels.vote_bytes(list(bufs), width, voted=voted, device=device, stream=st)

@@ -75,6 +75,10 @@ MATMUL_VARIANTS = (("mm_tc", "gpu-tc", mm_tc_body), ("mm_simt", "gpu-simt", mm_s
 # 3xBF16 keeps ~fp32 operand precision; single-pass TF32 rounds operands to
 # 10 mantissa bits (~5e-5 relative).  A passing vote commits SIMT's buffer.
 MATMUL_FIDELITY = {"mm_simt": 0, "mm_tc3x": 1, "mm_tc": 2}
+# dispatch order on a shared GPU (Runtime.attach_kernel cost): standalone
+# 4096^2 times 2.33 / 0.37 / 0.27 ms; the SIMT grid goes first
+# on the lead stream and the tensor-core replicas fill its last wave
+MATMUL_COST = {"mm_simt": 8.6, "mm_tc3x": 1.4, "mm_tc": 1.0}
 
 
 # ---- reference 1-D tasks ---------------------------------------------------------------
@@ -155,6 +159,7 @@ class Workload:
     input_fn: Callable = _uniform_input
     bind: Callable = _vector_bind
     fidelity: dict = field(default_factory=dict)     # kernel -> attach_kernel fidelity rank
+    cost: dict = field(default_factory=dict)         # kernel -> attach_kernel cost
 
     def make_input(self, size: int, rng):
         return self.input_fn(size, rng)
@@ -163,8 +168,9 @@ class Workload:
         task = runtime.declare_task(self.name, self.params, float_delta=float_delta)
         for kernel, kind, body in self.variants:
             if kinds is None or kind in kinds:
-                if self.fidelity:
-                    runtime.attach_kernel(task, kernel, kind, body, fidelity=self.fidelity.get(kernel, 0))
+                if self.fidelity or self.cost:
+                    runtime.attach_kernel(task, kernel, kind, body, fidelity=self.fidelity.get(kernel, 0),
+                                          cost=self.cost.get(kernel, 0.0))
                 else:
                     runtime.attach_kernel(task, kernel, kind, body)
         return task
@@ -211,7 +217,8 @@ _register(Workload("buggy-inc", "increment with a deterministic off-by-one bug i
                    oracle=_inc_oracle))
 _register(Workload("matmul", "C = A·B, fp32 n x n: tcgen05 TF32 / SIMT FP32 / tcgen05 3xBF16 variants",
                    list(MATMUL_VARIANTS), oracle=_matmul_oracle, params=MATMUL_PARAMS,
-                   input_fn=_matmul_input, bind=_matmul_bind, fidelity=MATMUL_FIDELITY))
+                   input_fn=_matmul_input, bind=_matmul_bind, fidelity=MATMUL_FIDELITY,
+                   cost=MATMUL_COST))
 
 
 def builtin_workloads() -> dict:

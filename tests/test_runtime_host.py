@@ -606,6 +606,49 @@ class TestCommitFidelity:
         assert got.tobytes() == want.tobytes()
 
 
+class TestDispatchCost:
+    """attach_kernel(cost=...) orders a round's launches longest first (the
+    lead replica on a shared GPU); without a cost on every variant the
+    measured mean runtimes order them, as before."""
+
+    def _rt(self, costs):
+        rt = hf.Runtime(hf.load_fleet(three_units()), hf.RuntimeConfig(serial_replicas=True),
+                        backend=HostBackend())
+        task = rt.declare_task("inc", IO)
+        calls = []
+
+        def body_of(k):
+            inner = _scaled_inc(1.0)
+
+            def body(ctx):
+                calls.append(k)
+                inner(ctx)
+            return body
+        for k in ("cpu", "gpu"):
+            rt.attach_kernel(task, f"inc_{k}", k, body_of(k), cost=costs.get(k, 0.0))
+        return rt, task, calls
+
+    @pytest.mark.parametrize("heavy", ["cpu", "gpu"])
+    def test_cost_orders_launches(self, heavy):
+        rt, task, calls = self._rt({heavy: 5.0, ("gpu" if heavy == "cpu" else "cpu"): 1.0})
+        _, o, a = args_for(rt)
+        for _ in range(3):
+            rep = rt.invoke(task, a, hf.Strategy(hf.StrategyKind.HET_DMR))
+            assert rep.success
+            assert calls[-2] == heavy, calls
+        assert len(calls) == 6
+
+    def test_negative_cost_rejected(self):
+        rt = hf.Runtime(hf.load_fleet(three_units()), hf.RuntimeConfig(), backend=HostBackend())
+        task = rt.declare_task("inc", IO)
+        with pytest.raises(hf.DeclarationError):
+            rt.attach_kernel(task, "inc_cpu", "cpu", _scaled_inc(1.0), cost=-1.0)
+
+    def test_matmul_workload_declares_costs(self):
+        from paper_1405_2912_b200 import workloads
+        assert max(workloads.MATMUL_COST, key=workloads.MATMUL_COST.get) == "mm_simt"
+
+
 # ---- learnt voter cost (VoterCostModel) ---------------------------------------------
 
 def test_voter_cost_model_fits_measured_line():

@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/simt_lab2 tools/simt_lab2.cu
+timeout 300 ./tools/simt_lab2 > gpurun_out/lab2_simt.jsonl 2>&1; echo lab2 rc=$?
+timeout 300 python tools/pipeline_lab.py 40 > gpurun_out/pipeline_lab.jsonl 2>&1; echo pipe rc=$?
+cat gpurun_out/lab2_simt.jsonl gpurun_out/pipeline_lab.jsonl

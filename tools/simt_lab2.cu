@@ -1,0 +1,333 @@
+// SIMT GEMM lab 2 (not product code): 8 x 16 outputs per thread, 128-thread
+// CTAs on the product's 128 x 128 CTA tile (two CTAs per SM, as the product),
+// so each thread holds 64 accumulator pairs and reads 6 LDS.128 per 64 FFMA2
+// (the product: 4 per 32).  Chain accumulation in ascending k, so results
+// are bit-identical to the product's single-chain kernel (sgemm_v here).
+// Optional blocked accumulation (CH k-tiles per chain, running totals in
+// shared memory) as the product kernel does.
+//   nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/simt_lab2 tools/simt_lab2.cu
+#include <cstdio>
+#include <cstdint>
+#include <cstring>
+#include <cstdlib>
+#include <vector>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void ffma2(unsigned long long& d, unsigned long long a, unsigned long long b) {
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+                 "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// product shape (single chain): 256 threads, 8x8 per thread
+template <int BK, int ST>
+__global__ void __launch_bounds__(256, 2)
+sgemm_v(const float* __restrict__ At, const float* __restrict__ B, float* __restrict__ C, int M, int N, int K) {
+    constexpr int BM = 128, BN = 128;
+    extern __shared__ __align__(16) float sm[];
+    float* As = sm;
+    float* Bs = sm + ST * BK * BM;
+    const int t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31;
+    const int ty = (warp >> 1) * 4 + (lane >> 3);
+    const int tx = (warp & 1) * 8 + (lane & 7);
+    const int tiles_n = N / BN, tiles_m = M / BM;
+    const int group = 16, bid = blockIdx.x, per_group = group * tiles_n;
+    const int g = bid / per_group, first_m = g * group;
+    const int gm = min(tiles_m - first_m, group);
+    const int tm = first_m + (bid % per_group) % gm, tn = (bid % per_group) / gm;
+    const int m0 = tm * BM, n0 = tn * BN;
+    const int c_row = t >> 5, c_col = (t & 31) * 4;
+    const float* Ag = At + static_cast<long long>(c_row) * M + m0 + c_col;
+    const float* Bg = B + static_cast<long long>(c_row) * N + n0 + c_col;
+    auto issue = [&](int kt, int stage) {
+        const long long ka = static_cast<long long>(kt) * BK * M;
+        const long long kb = static_cast<long long>(kt) * BK * N;
+        float* as = As + stage * BK * BM + c_row * BM + c_col;
+        float* bs = Bs + stage * BK * BN + c_row * BN + c_col;
+#pragma unroll
+        for (int r = 0; r < BK; r += 8) {
+            cp_async16(as + r * BM, Ag + ka + static_cast<long long>(r) * M);
+            cp_async16(bs + r * BN, Bg + kb + static_cast<long long>(r) * N);
+        }
+    };
+    unsigned long long acc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0ull;
+    const int nk = K / BK;
+#pragma unroll
+    for (int s = 0; s < ST - 1; ++s) {
+        if (s < nk) issue(s, s);
+        cp_async_commit();
+    }
+    for (int kt = 0; kt < nk; ++kt) {
+        cp_async_wait<ST - 2>();
+        __syncthreads();
+        {
+            const int nt = kt + ST - 1;
+            if (nt < nk) issue(nt, nt % ST);
+            cp_async_commit();
+        }
+        const float* as = As + (kt % ST) * BK * BM;
+        const float* bs = Bs + (kt % ST) * BK * BN;
+        float4 fa[2][2], fb[2][2];
+        fa[0][0] = *reinterpret_cast<const float4*>(as + ty * 4);
+        fa[0][1] = *reinterpret_cast<const float4*>(as + 64 + ty * 4);
+        fb[0][0] = *reinterpret_cast<const float4*>(bs + tx * 4);
+        fb[0][1] = *reinterpret_cast<const float4*>(bs + 64 + tx * 4);
+#pragma unroll
+        for (int k = 0; k < BK; ++k) {
+            const int cur = k & 1, nxt = cur ^ 1;
+            if (k + 1 < BK) {
+                fa[nxt][0] = *reinterpret_cast<const float4*>(as + (k + 1) * BM + ty * 4);
+                fa[nxt][1] = *reinterpret_cast<const float4*>(as + (k + 1) * BM + 64 + ty * 4);
+                fb[nxt][0] = *reinterpret_cast<const float4*>(bs + (k + 1) * BN + tx * 4);
+                fb[nxt][1] = *reinterpret_cast<const float4*>(bs + (k + 1) * BN + 64 + tx * 4);
+            }
+            const float a[8] = {fa[cur][0].x, fa[cur][0].y, fa[cur][0].z, fa[cur][0].w,
+                                fa[cur][1].x, fa[cur][1].y, fa[cur][1].z, fa[cur][1].w};
+            const unsigned long long b[4] = {pack2(fb[cur][0].x, fb[cur][0].y), pack2(fb[cur][0].z, fb[cur][0].w),
+                                             pack2(fb[cur][1].x, fb[cur][1].y), pack2(fb[cur][1].z, fb[cur][1].w)};
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const unsigned long long ai = pack2(a[i], a[i]);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) ffma2(acc[i][j], ai, b[j]);
+            }
+        }
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int row = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+        float* crow = C + static_cast<long long>(row) * N + n0;
+        *reinterpret_cast<ulonglong2*>(crow + tx * 4) = make_ulonglong2(acc[i][0], acc[i][1]);
+        *reinterpret_cast<ulonglong2*>(crow + 64 + tx * 4) = make_ulonglong2(acc[i][2], acc[i][3]);
+    }
+}
+
+// 8 (m) x 16 (n) per thread, 128 threads.  Warp = 4 (m) x 8 (n) lanes; the 4
+// warps stack along m.  Thread rows: ty*4 + {0..3} and 64 + ty*4 + {0..3}
+// (ty = warp*4 + lane/8 in 0..15); columns c*32 + tx*4 + {0..3}, c = 0..3
+// (tx = lane%8).  Every LDS.128 of a warp touches 4 (A) or 8 (B) distinct
+// 16-byte words: one wavefront each.
+template <int BK, int ST, int CH, int ORDER>
+__global__ void __launch_bounds__(128, 2)
+sgemm_8x16(const float* __restrict__ At, const float* __restrict__ B, float* __restrict__ C, int M, int N, int K) {
+    constexpr int BM = 128, BN = 128, NT = 128;
+    extern __shared__ __align__(16) float sm[];
+    float* As = sm;
+    float* Bs = sm + ST * BK * BM;
+    ulonglong2* Tot = reinterpret_cast<ulonglong2*>(Bs + ST * BK * BN);   // [32][128] x 16 B
+    const int t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31;
+    const int ty = warp * 4 + (lane >> 3);
+    const int tx = lane & 7;
+    const int tiles_n = N / BN, tiles_m = M / BM;
+    const int group = 16, bid = blockIdx.x, per_group = group * tiles_n;
+    const int g = bid / per_group, first_m = g * group;
+    const int gm = min(tiles_m - first_m, group);
+    const int tm = first_m + (bid % per_group) % gm, tn = (bid % per_group) / gm;
+    const int m0 = tm * BM, n0 = tn * BN;
+    // copy: each k-row of a tile is 32 chunks of 16 B; thread t moves chunk
+    // (t & 31) of rows (t >> 5) + 4r
+    const int c_row = t >> 5, c_col = (t & 31) * 4;
+    const float* Ag = At + static_cast<long long>(c_row) * M + m0 + c_col;
+    const float* Bg = B + static_cast<long long>(c_row) * N + n0 + c_col;
+    auto issue = [&](int kt, int stage) {
+        const long long ka = static_cast<long long>(kt) * BK * M;
+        const long long kb = static_cast<long long>(kt) * BK * N;
+        float* as = As + stage * BK * BM + c_row * BM + c_col;
+        float* bs = Bs + stage * BK * BN + c_row * BN + c_col;
+#pragma unroll
+        for (int r = 0; r < BK; r += 4) {
+            cp_async16(as + r * BM, Ag + ka + static_cast<long long>(r) * M);
+            cp_async16(bs + r * BN, Bg + kb + static_cast<long long>(r) * N);
+        }
+    };
+    unsigned long long acc[8][8];   // [row i][col pair j]: cols (j>>1)*32 + tx*4 + 2*(j&1)
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0ull;
+    if constexpr (CH > 0) {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) Tot[q * NT + t] = make_ulonglong2(0ull, 0ull);
+    }
+    const int nk = K / BK;
+#pragma unroll
+    for (int s = 0; s < ST - 1; ++s) {
+        if (s < nk) issue(s, s);
+        cp_async_commit();
+    }
+    for (int kt = 0; kt < nk; ++kt) {
+        cp_async_wait<ST - 2>();
+        __syncthreads();
+        {
+            const int nt = kt + ST - 1;
+            if (nt < nk) issue(nt, nt % ST);
+            cp_async_commit();
+        }
+        const float* as = As + (kt % ST) * BK * BM;
+        const float* bs = Bs + (kt % ST) * BK * BN;
+        float4 fa[2][2], fb[2][4];
+        fa[0][0] = *reinterpret_cast<const float4*>(as + ty * 4);
+        fa[0][1] = *reinterpret_cast<const float4*>(as + 64 + ty * 4);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) fb[0][c] = *reinterpret_cast<const float4*>(bs + c * 32 + tx * 4);
+#pragma unroll
+        for (int k = 0; k < BK; ++k) {
+            const int cur = k & 1, nxt = cur ^ 1;
+            if (k + 1 < BK) {
+                fa[nxt][0] = *reinterpret_cast<const float4*>(as + (k + 1) * BM + ty * 4);
+                fa[nxt][1] = *reinterpret_cast<const float4*>(as + (k + 1) * BM + 64 + ty * 4);
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    fb[nxt][c] = *reinterpret_cast<const float4*>(bs + (k + 1) * BN + c * 32 + tx * 4);
+            }
+            const float a[8] = {fa[cur][0].x, fa[cur][0].y, fa[cur][0].z, fa[cur][0].w,
+                                fa[cur][1].x, fa[cur][1].y, fa[cur][1].z, fa[cur][1].w};
+            unsigned long long b[8];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                b[2 * c] = pack2(fb[cur][c].x, fb[cur][c].y);
+                b[2 * c + 1] = pack2(fb[cur][c].z, fb[cur][c].w);
+            }
+            if (ORDER == 0) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const unsigned long long ai = pack2(a[i], a[i]);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) ffma2(acc[i][j], ai, b[j]);
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) ffma2(acc[i][j], pack2(a[i], a[i]), b[j]);
+            }
+        }
+        if constexpr (CH > 0) {
+            if ((kt + 1) % CH == 0 || kt + 1 == nk) {
+                const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(Tot + t));
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        asm volatile(
+                            "{\n\t.reg .b64 t0, t1, t2, t3;\n\t"
+                            "ld.shared.v2.b64 {t0, t1}, [%4];\n\t"
+                            "ld.shared.v2.b64 {t2, t3}, [%4+2048];\n\t"
+                            "add.rn.f32x2 t0, t0, %0;\n\tadd.rn.f32x2 t1, t1, %1;\n\t"
+                            "add.rn.f32x2 t2, t2, %2;\n\tadd.rn.f32x2 t3, t3, %3;\n\t"
+                            "st.shared.v2.b64 [%4], {t0, t1};\n\t"
+                            "st.shared.v2.b64 [%4+2048], {t2, t3};\n\t"
+                            "mov.b64 %0, 0;\n\tmov.b64 %1, 0;\n\tmov.b64 %2, 0;\n\tmov.b64 %3, 0;\n\t}"
+                            : "+l"(acc[i][4 * h]), "+l"(acc[i][4 * h + 1]), "+l"(acc[i][4 * h + 2]),
+                              "+l"(acc[i][4 * h + 3])
+                            : "r"(base + static_cast<uint32_t>((4 * i + 2 * h) * NT * 16))
+                            : "memory");
+            }
+        }
+    }
+    cp_async_wait<0>();
+    if constexpr (CH > 0) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const ulonglong2 v = Tot[(4 * i + q) * NT + t];
+                acc[i][2 * q] = v.x;
+                acc[i][2 * q + 1] = v.y;
+            }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int row = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+        float* crow = C + static_cast<long long>(row) * N + n0 + tx * 4;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            *reinterpret_cast<ulonglong2*>(crow + c * 32) = make_ulonglong2(acc[i][2 * c], acc[i][2 * c + 1]);
+    }
+}
+
+template <typename Kern>
+static void run(const char* name, Kern k, int threads, int smem, const float* At, const float* B, float* C,
+                const float* Cref, int n, size_t bytes) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    const int tiles = (n / 128) * (n / 128);
+    for (int i = 0; i < 3; ++i) k<<<tiles, threads, smem>>>(At, B, C, n, n, n);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e9, sum = 0;
+    for (int i = 0; i < 20; ++i) {
+        cudaEventRecord(e0);
+        k<<<tiles, threads, smem>>>(At, B, C, n, n, n);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        best = ms < best ? ms : best;
+        sum += ms;
+    }
+    const char* same = "null";
+    if (Cref) {
+        std::vector<float> h(bytes / 4), r(bytes / 4);
+        cudaMemcpy(h.data(), C, bytes, cudaMemcpyDeviceToHost);
+        cudaMemcpy(r.data(), Cref, bytes, cudaMemcpyDeviceToHost);
+        same = memcmp(h.data(), r.data(), bytes) == 0 ? "true" : "false";
+    }
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, threads, smem);
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, k);
+    double fl = 2.0 * n * n * (double)n;
+    printf("{\"variant\": \"%s\", \"regs\": %d, \"occ\": %d, \"smem\": %d, \"ms_min\": %.4f, \"ms_mean\": %.4f, "
+           "\"tflops\": %.2f, \"bit_identical\": %s, \"err\": \"%s\"}\n",
+           name, fa.numRegs, occ, smem, best, sum / 20, fl / (best * 1e-3) / 1e12, same,
+           cudaGetErrorString(cudaGetLastError()));
+    fflush(stdout);
+}
+
+__global__ void init(float* p, size_t n, uint32_t seed) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        uint32_t x = (uint32_t)i * 2654435761u ^ seed;
+        x ^= x >> 13; x *= 0x5bd1e995u; x ^= x >> 15;
+        p[i] = 1.0f + (x >> 8) * (1.0f / 16777216.0f);
+    }
+}
+
+int main(int argc, char** argv) {
+    int n = argc > 1 ? atoi(argv[1]) : 4096;
+    size_t bytes = (size_t)n * n * 4;
+    float *At, *B, *C, *C0, *C1;
+    cudaMalloc(&At, bytes); cudaMalloc(&B, bytes); cudaMalloc(&C, bytes); cudaMalloc(&C0, bytes);
+    cudaMalloc(&C1, bytes);
+    init<<<1184, 256>>>(At, (size_t)n * n, 1);
+    init<<<1184, 256>>>(B, (size_t)n * n, 2);
+    const int ring3 = 3 * 16 * 256 * 4, ring4 = 4 * 16 * 256 * 4;
+    run("product chain 8x8 k16s3", sgemm_v<16, 3>, 256, ring3, At, B, C0, nullptr, n, bytes);
+    run("8x16 chain k16s3 i-outer", sgemm_8x16<16, 3, 0, 0>, 128, ring3, At, B, C, C0, n, bytes);
+    run("8x16 chain k16s3 j-outer", sgemm_8x16<16, 3, 0, 1>, 128, ring3, At, B, C, C0, n, bytes);
+    run("8x16 chain k16s4 i-outer", sgemm_8x16<16, 4, 0, 0>, 128, ring4, At, B, C, C0, n, bytes);
+    run("8x16 chain k8s4 i-outer", sgemm_8x16<8, 4, 0, 0>, 128, 4 * 8 * 256 * 4, At, B, C, C0, n, bytes);
+    run("8x16 chain k32s2 i-outer", sgemm_8x16<32, 2, 0, 0>, 128, 2 * 32 * 256 * 4, At, B, C, C0, n, bytes);
+    run("8x16 blocked32 k16s3 i-outer", sgemm_8x16<16, 3, 32, 0>, 128, ring3 + 32 * 128 * 16, At, B, C1, nullptr,
+        n, bytes);
+    run("product chain 8x8 k16s3 (again)", sgemm_v<16, 3>, 256, ring3, At, B, C, C0, n, bytes);
+    return 0;
+}
