@@ -44,6 +44,8 @@ _VIEW_DTYPES: dict = {}     # (ValueType, width) -> (numpy dtype, torch dtype) o
 # a finished task's vote is dispatched ahead of the next task's SIMT CTAs.
 VOTE_PRIORITY = -2
 _VOTE_STREAM = os.environ.get("HETFT_VOTE_STREAM", "1") != "0"
+# the device's compute stream (checkpoints, copies-in, fills): A/B knob
+COMPUTE_PRIORITY = int(os.environ.get("HETFT_COMPUTE_PRIORITY", "0"))
 
 
 class CudaBackend:
@@ -71,7 +73,7 @@ class CudaBackend:
         with self._lock:
             s = self._streams.get(device)
             if s is None:
-                s = torch.cuda.Stream(device=device)
+                s = torch.cuda.Stream(device=device, priority=COMPUTE_PRIORITY)
                 self._streams[device] = s
         return s
 

@@ -9,13 +9,11 @@
 //
 // Fast path (M%128 == N%128 == 0, K%32 == 0, 16B-aligned): A is transposed
 // once by a tiled pre-pass (~2|A| bytes, ~1% of the GEMM) so both operands
-// stream as contiguous k-rows; 128x128x16 CTA tile, 256 threads, 8x8 outputs
-// per thread as 2x2 blocks of 4x4, cp.async 3-stage smem ring, one barrier
-// per k-tile, register double-buffered fragments, two CTAs per SM; the
-// outer product issues packed FFMA2 (fma.rn.f32x2): every output is still an
-// fp32 FMA chain in ascending k, so results equal the FFMA formulation bit
-// for bit.  Warps are laid out 4x2 over the
-// 16x16 thread grid so each LDS.128 of A and of B is one wavefront.
+// stream as contiguous k-rows; 128x128x16 CTA tile, 128 threads, 8x16
+// outputs per thread, cp.async 3-stage smem ring, one barrier per k-tile,
+// register double-buffered fragments, two CTAs per SM; the outer product
+// issues packed FFMA2 (fma.rn.f32x2): every output is still an fp32 FMA
+// chain in ascending k, so results equal the FFMA formulation bit for bit.
 // Generic path: 16x16 bounds-checked tiles for ragged shapes.
 #include "common.cuh"
 
@@ -53,36 +51,49 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// 128x128x16 CTA tile, 256 threads, 8x8 outputs per thread.  Operands are
-// A^T (K x M, from the transpose pre-pass) and B (K x N): both k-tiles are
-// 16 rows of 512 contiguous bytes, streamed by cp.async into a 3-stage smem
-// ring without staging registers; fragments for k+1 are read from smem
-// while k is multiplied.  <= 128 registers: two CTAs (16 warps) per SM hide
-// each other's barrier and latency stalls.
+// 128x128x16 CTA tile, 128 threads, 8 (m) x 16 (n) outputs per thread (r2;
+// round 1: 256 threads x 8x8).  Operands are A^T (K x M, from the transpose
+// pre-pass) and B (K x N): both k-tiles are 16 rows of 512 contiguous bytes,
+// streamed by cp.async into a 3-stage smem ring without staging registers;
+// fragments for k+1 are read from smem while k is multiplied.  Per k-step a
+// thread reads 2 LDS.128 of A and 4 of B for 64 FFMA2 (8x8/256 threads: 4
+// for 32) and issues them column-pair-outer: each b pair is reused by 8
+// consecutive FFMA2.  ~254 registers, two CTAs (8 warps) per SM.  Warp =
+// 4 (m) x 8 (n) lanes, the 4 warps stacked along m; thread rows ty*4 + {0..3}
+// and 64 + ty*4 + {0..3} (ty = warp*4 + lane/8), columns c*32 + tx*4 + {0..3}
+// for c = 0..3 (tx = lane%8): every LDS.128 of a warp touches 4 (A) or 8 (B)
+// distinct 16-byte words, one wavefront each.  Measured against the 8x8
+// layout at 4096^3 (tools/simt_lab2.cu, profiles/r02_simt_lab2b.jsonl):
+// blocked accumulation 2.175 ms (the 8x8 kernel's single chain: 2.172, its
+// blocked form ~2.30); the a-scalar-outer issue order of the same layout
+// 2.285.  Results are bit-identical to the 8x8 kernel (same chains, same
+// chunk sums).
 //
 // Blocked accumulation (CH > 0, the default): the fp32 FMA chain of an
 // output runs over CH k-tiles (CH*16 products) only; the chunk's sum is then
-// added (one rounding) into a running total that lives in shared memory, 64
-// floats per thread laid out [16][256] x 16 B (conflict-free 128-bit
+// added (one rounding) into a running total that lives in shared memory, 128
+// floats per thread laid out [32][128] x 16 B (conflict-free 128-bit
 // accesses), and the register accumulators restart at zero — the blocked
 // summation an optimised CPU sgemm does.  At 4096^2 the max relative error
 // against the binary64 product is 7.1e-7 (numpy/OpenBLAS fp32, the
 // reference body's arithmetic: 5.5e-7) instead of 5.4e-6 for one 4096-long
-// chain, for 64 KB more smem per CTA (112 KB: still two CTAs per SM) and
-// ~5% of kernel time.  CH = 0: one chain in ascending k (A/B only).
+// chain, for 64 KB more smem per CTA (112 KB: still two CTAs per SM).
+// CH = 0: one chain in ascending k (A/B only).
+constexpr int SGEMM_THREADS = 128;
 template <int CH>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(SGEMM_THREADS, 2)
 sgemm_128x128(const float* __restrict__ At, const float* __restrict__ B, float* __restrict__ C,
               int M, int N, int K, int group) {
+    constexpr int NT = SGEMM_THREADS;
     extern __shared__ __align__(16) float sm[];
     float* As = sm;                                   // [S][SB_K][SB_M]
     float* Bs = sm + S_STAGES * SB_K * SB_M;          // [S][SB_K][SB_N]
-    ulonglong2* Tot = reinterpret_cast<ulonglong2*>(Bs + S_STAGES * SB_K * SB_N);   // [16][256]
+    ulonglong2* Tot = reinterpret_cast<ulonglong2*>(Bs + S_STAGES * SB_K * SB_N);   // [32][NT]
 
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;
-    const int ty = (warp >> 1) * 4 + (lane >> 3);  // 0..15
-    const int tx = (warp & 1) * 8 + (lane & 7);    // 0..15
+    const int ty = warp * 4 + (lane >> 3);   // 0..15
+    const int tx = lane & 7;                 // 0..7
 
     // grouped tile order: consecutive CTAs share B column panels in L2
     const int tiles_n = N / SB_N;
@@ -97,68 +108,60 @@ sgemm_128x128(const float* __restrict__ At, const float* __restrict__ B, float* 
     const int m0 = tm * SB_M, n0 = tn * SB_N;
 
     // copy mapping: each of the 16 k-rows is 32 chunks of 16 B per operand;
-    // thread t moves chunk (t & 31) of rows (t >> 5) and (t >> 5) + 8
+    // thread t moves chunk (t & 31) of rows (t >> 5) + {0, 4, 8, 12}
     const int c_row = t >> 5, c_col = (t & 31) * 4;
     const float* Ag = At + static_cast<long long>(c_row) * M + m0 + c_col;
     const float* Bg = B + static_cast<long long>(c_row) * N + n0 + c_col;
-    const long long a8 = 8LL * M, b8 = 8LL * N;
+    const long long a4 = 4LL * M, b4 = 4LL * N;
 
     auto issue = [&](int kt, int stage) {
         const long long ka = static_cast<long long>(kt) * SB_K * M;
         const long long kb = static_cast<long long>(kt) * SB_K * N;
         float* as = As + stage * SB_K * SB_M + c_row * SB_M + c_col;
         float* bs = Bs + stage * SB_K * SB_N + c_row * SB_N + c_col;
-        cp_async16(as, Ag + ka);
-        cp_async16(as + 8 * SB_M, Ag + ka + a8);
-        cp_async16(bs, Bg + kb);
-        cp_async16(bs + 8 * SB_N, Bg + kb + b8);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            cp_async16(as + r * 4 * SB_M, Ag + ka + r * a4);
+            cp_async16(bs + r * 4 * SB_N, Bg + kb + r * b4);
+        }
     };
 
-    // acc[i][j] holds the output pair (2j, 2j+1) of row i
-    unsigned long long acc[8][4];
+    // acc[i][j] holds the output pair of row i, columns (j>>1)*32 + tx*4 + 2*(j&1) + {0, 1}
+    unsigned long long acc[8][8];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0ull;
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0ull;
 
     if constexpr (CH > 0) {
 #pragma unroll
-        for (int q = 0; q < 16; ++q) Tot[q * 256 + t] = make_ulonglong2(0ull, 0ull);
+        for (int q = 0; q < 32; ++q) Tot[q * NT + t] = make_ulonglong2(0ull, 0ull);
     }
-    // running total += chunk sum (acc pair (i, j) <-> Tot[q = 2i + j/2], half
-    // j&1), then the chain restarts at zero.  Written in asm that updates
-    // the accumulators in place, called behind a uniform branch from the
-    // single k-tile loop: a C++ restart at zero (or a nested chunk loop) gave
-    // every accumulator a second definition, ptxas assigned them different
-    // registers and the loop back-edge grew ~32 MOVs per k-tile (+4.5%
-    // time).  Of the loop shapes tried (tools/simt_ab.py,
-    // profiles/r02_simt_ab_fv.jsonl) this one is fastest: +3.7% over the
-    // single chain (branch inside the asm +4.2%, two k-tiles per test +5.8%,
-    // a countdown instead of the modulo +4.2%).
+    // running total += chunk sum (acc pairs (i, 4h..4h+3) <-> Tot[q = 4i + 2h,
+    // 4i + 2h + 1]), then the chain restarts at zero.  Written in asm that
+    // updates the accumulators in place, called behind a uniform branch from
+    // the single k-tile loop: a C++ restart at zero (or a nested chunk loop)
+    // gave every accumulator a second definition, ptxas assigned them
+    // different registers and the loop back-edge grew MOVs (round 2 A/B,
+    // tools/simt_ab.py, profiles/r02_simt_ab_fv.jsonl).
     const uint32_t tot_s = static_cast<uint32_t>(__cvta_generic_to_shared(Tot + t));
     auto flush = [&]() {
 #pragma unroll
-        for (int i = 0; i < 8; i += 2)
-            asm volatile(
-                "{\n\t.reg .b64 t0, t1, t2, t3, t4, t5, t6, t7;\n\t"
-                "ld.shared.v2.b64 {t0, t1}, [%8];\n\t"
-                "ld.shared.v2.b64 {t2, t3}, [%8+4096];\n\t"
-                "ld.shared.v2.b64 {t4, t5}, [%8+8192];\n\t"
-                "ld.shared.v2.b64 {t6, t7}, [%8+12288];\n\t"
-                "add.rn.f32x2 t0, t0, %0;\n\tadd.rn.f32x2 t1, t1, %1;\n\t"
-                "add.rn.f32x2 t2, t2, %2;\n\tadd.rn.f32x2 t3, t3, %3;\n\t"
-                "add.rn.f32x2 t4, t4, %4;\n\tadd.rn.f32x2 t5, t5, %5;\n\t"
-                "add.rn.f32x2 t6, t6, %6;\n\tadd.rn.f32x2 t7, t7, %7;\n\t"
-                "st.shared.v2.b64 [%8], {t0, t1};\n\t"
-                "st.shared.v2.b64 [%8+4096], {t2, t3};\n\t"
-                "st.shared.v2.b64 [%8+8192], {t4, t5};\n\t"
-                "st.shared.v2.b64 [%8+12288], {t6, t7};\n\t"
-                "mov.b64 %0, 0;\n\tmov.b64 %1, 0;\n\tmov.b64 %2, 0;\n\tmov.b64 %3, 0;\n\t"
-                "mov.b64 %4, 0;\n\tmov.b64 %5, 0;\n\tmov.b64 %6, 0;\n\tmov.b64 %7, 0;\n\t}"
-                : "+l"(acc[i][0]), "+l"(acc[i][1]), "+l"(acc[i][2]), "+l"(acc[i][3]),
-                  "+l"(acc[i + 1][0]), "+l"(acc[i + 1][1]), "+l"(acc[i + 1][2]), "+l"(acc[i + 1][3])
-                : "r"(tot_s + static_cast<uint32_t>(2 * i * 256 * 16))
-                : "memory");
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+                asm volatile(
+                    "{\n\t.reg .b64 t0, t1, t2, t3;\n\t"
+                    "ld.shared.v2.b64 {t0, t1}, [%4];\n\t"
+                    "ld.shared.v2.b64 {t2, t3}, [%4+2048];\n\t"
+                    "add.rn.f32x2 t0, t0, %0;\n\tadd.rn.f32x2 t1, t1, %1;\n\t"
+                    "add.rn.f32x2 t2, t2, %2;\n\tadd.rn.f32x2 t3, t3, %3;\n\t"
+                    "st.shared.v2.b64 [%4], {t0, t1};\n\t"
+                    "st.shared.v2.b64 [%4+2048], {t2, t3};\n\t"
+                    "mov.b64 %0, 0;\n\tmov.b64 %1, 0;\n\tmov.b64 %2, 0;\n\tmov.b64 %3, 0;\n\t}"
+                    : "+l"(acc[i][4 * h]), "+l"(acc[i][4 * h + 1]), "+l"(acc[i][4 * h + 2]), "+l"(acc[i][4 * h + 3])
+                    : "r"(tot_s + static_cast<uint32_t>((4 * i + 2 * h) * NT * 16))
+                    : "memory");
     };
     const int nk = K / SB_K;
     pdl_wait();     // launched with PDL behind the A^T pre-pass: At is complete from here
@@ -178,31 +181,36 @@ sgemm_128x128(const float* __restrict__ At, const float* __restrict__ B, float* 
         }
         const float* as = As + (kt % S_STAGES) * SB_K * SB_M;
         const float* bs = Bs + (kt % S_STAGES) * SB_K * SB_N;
-        float4 fa[2][2], fb[2][2];
+        float4 fa[2][2], fb[2][4];
         fa[0][0] = *reinterpret_cast<const float4*>(as + ty * 4);
         fa[0][1] = *reinterpret_cast<const float4*>(as + 64 + ty * 4);
-        fb[0][0] = *reinterpret_cast<const float4*>(bs + tx * 4);
-        fb[0][1] = *reinterpret_cast<const float4*>(bs + 64 + tx * 4);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) fb[0][c] = *reinterpret_cast<const float4*>(bs + c * 32 + tx * 4);
 #pragma unroll
         for (int k = 0; k < SB_K; ++k) {
             const int cur = k & 1, nxt = cur ^ 1;
             if (k + 1 < SB_K) {
                 fa[nxt][0] = *reinterpret_cast<const float4*>(as + (k + 1) * SB_M + ty * 4);
                 fa[nxt][1] = *reinterpret_cast<const float4*>(as + (k + 1) * SB_M + 64 + ty * 4);
-                fb[nxt][0] = *reinterpret_cast<const float4*>(bs + (k + 1) * SB_N + tx * 4);
-                fb[nxt][1] = *reinterpret_cast<const float4*>(bs + (k + 1) * SB_N + 64 + tx * 4);
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    fb[nxt][c] = *reinterpret_cast<const float4*>(bs + (k + 1) * SB_N + c * 32 + tx * 4);
             }
             const float a[8] = {fa[cur][0].x, fa[cur][0].y, fa[cur][0].z, fa[cur][0].w,
                                 fa[cur][1].x, fa[cur][1].y, fa[cur][1].z, fa[cur][1].w};
             // b pairs are the LDS.128 destination registers, already adjacent
-            const unsigned long long b[4] = {pack2(fb[cur][0].x, fb[cur][0].y), pack2(fb[cur][0].z, fb[cur][0].w),
-                                             pack2(fb[cur][1].x, fb[cur][1].y), pack2(fb[cur][1].z, fb[cur][1].w)};
+            unsigned long long b[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const unsigned long long ai = pack2(a[i], a[i]);   // folded into FFMA2's scalar operand
-#pragma unroll
-                for (int j = 0; j < 4; ++j) ffma2(acc[i][j], ai, b[j]);
+            for (int c = 0; c < 4; ++c) {
+                b[2 * c] = pack2(fb[cur][c].x, fb[cur][c].y);
+                b[2 * c + 1] = pack2(fb[cur][c].z, fb[cur][c].w);
             }
+            // column-pair-outer: the b pair stays in the operand reuse cache
+            // across 8 FFMA2 (a scalars folded into FFMA2's broadcast operand)
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) ffma2(acc[i][j], pack2(a[i], a[i]), b[j]);
         }
     };
     for (int kt = 0; kt < nk; ++kt) {
@@ -216,19 +224,20 @@ sgemm_128x128(const float* __restrict__ At, const float* __restrict__ B, float* 
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const ulonglong2 v = Tot[(2 * i + h) * 256 + t];
-                acc[i][2 * h] = v.x;
-                acc[i][2 * h + 1] = v.y;
+            for (int q = 0; q < 4; ++q) {
+                const ulonglong2 v = Tot[(4 * i + q) * NT + t];
+                acc[i][2 * q] = v.x;
+                acc[i][2 * q + 1] = v.y;
             }
     }
 
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         const int row = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
-        float* crow = C + static_cast<long long>(row) * N + n0;
-        *reinterpret_cast<ulonglong2*>(crow + tx * 4) = make_ulonglong2(acc[i][0], acc[i][1]);
-        *reinterpret_cast<ulonglong2*>(crow + 64 + tx * 4) = make_ulonglong2(acc[i][2], acc[i][3]);
+        float* crow = C + static_cast<long long>(row) * N + n0 + tx * 4;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            *reinterpret_cast<ulonglong2*>(crow + c * 32) = make_ulonglong2(acc[i][2 * c], acc[i][2 * c + 1]);
     }
 }
 
@@ -238,7 +247,7 @@ sgemm_128x128(const float* __restrict__ At, const float* __restrict__ B, float* 
 // 4.5e-7 but the flushes' smem traffic adds another 2%; CH 64: 1.3e-6, 2.336 ms.
 constexpr int SGEMM_CH = 32;
 constexpr int SGEMM_SMEM_RING = S_STAGES * SB_K * (SB_M + SB_N) * 4;   // 48 KB
-constexpr int SGEMM_SMEM = SGEMM_SMEM_RING + 16 * 256 * 16;            // + 64 KB running totals
+constexpr int SGEMM_SMEM = SGEMM_SMEM_RING + 32 * SGEMM_THREADS * 16;   // + 64 KB running totals
 // Co-scheduled with the tensor-core replica (HF_GEMM_COSCHEDULE): each CTA
 // reserves 100 KB although it uses 48 KB.  Two SIMT CTAs still fit an SM,
 // and when one retires the space it frees takes one TC CTA (2-stage shape,
@@ -386,7 +395,7 @@ extern "C" int hf_gemm_simt(const float* A, const float* B, float* C, int M, int
             // by default: co-scheduled with a TC replica the TC GEMM then got
             // SMs at the start of the SIMT grid, 2.46 -> 2.49 ms per DMR round
             HF_CUDA_CHECK(hf::launch_pdl(hf::transpose_a, dim3(K / 32, M / 32), dim3(256), 0, st, A, At, M, K));
-            HF_CUDA_CHECK(hf::launch_pdl(kern, dim3(tiles), dim3(256), smem, st, At, B, C, M, N, K,
+            HF_CUDA_CHECK(hf::launch_pdl(kern, dim3(tiles), dim3(hf::SGEMM_THREADS), smem, st, At, B, C, M, N, K,
                                          hf::sgemm_group()));
         } else if (hf::side_prepass()) {
             // default: the pre-pass on the device's greatest-priority side
@@ -401,7 +410,7 @@ extern "C" int hf_gemm_simt(const float* A, const float* B, float* C, int M, int
             HF_CUDA_CHECK(hf::begin_side_launch(side, st, &ps));
             hf::transpose_a<<<dim3(K / 32, M / 32), 256, 0, ps>>>(A, At, M, K);
             HF_CUDA_CHECK(hf::end_side_launch(side, st));
-            kern<<<tiles, 256, smem, st>>>(At, B, C, M, N, K, hf::sgemm_group());
+            kern<<<tiles, hf::SGEMM_THREADS, smem, st>>>(At, B, C, M, N, K, hf::sgemm_group());
         } else {
             // HF_SIMT_SIDE_PREPASS=0: pre-pass and GEMM in stream order on the
             // caller's stream (no event gap).  Co-scheduled, the TC pre-pass
@@ -409,7 +418,7 @@ extern "C" int hf_gemm_simt(const float* A, const float* B, float* C, int M, int
             // the SIMT grid, even with the lead stream at the greatest priority
             // (2.44 -> 2.57 ms per DMR round)
             hf::transpose_a<<<dim3(K / 32, M / 32), 256, 0, st>>>(A, At, M, K);
-            kern<<<tiles, 256, smem, st>>>(At, B, C, M, N, K, hf::sgemm_group());
+            kern<<<tiles, hf::SGEMM_THREADS, smem, st>>>(At, B, C, M, N, K, hf::sgemm_group());
         }
     } else {
         dim3 grid((N + 15) / 16, (M + 15) / 16);

@@ -17,7 +17,8 @@ import bench  # noqa: E402
 from paper_1405_2912_b200 import executor as ex  # noqa: E402
 
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 40
-sys.argv = [sys.argv[0], "--steps", str(steps)]
+depth = sys.argv[sys.argv.index("--depth") + 1] if "--depth" in sys.argv else "1"
+sys.argv = [sys.argv[0], "--steps", str(steps), "--depth", depth]
 args = bench.parse()
 hf, rt, task = bench.build_runtime(0, 0.05, 1)
 leads = []

@@ -263,6 +263,174 @@ sgemm_8x16(const float* __restrict__ At, const float* __restrict__ B, float* __r
     }
 }
 
+
+// A read row-major (no A^T pre-pass): each k-tile of A (128 rows x 16 k) is
+// loaded by LDG.128 into registers one k-tile ahead (lane = row, 4 chunks of
+// 4 k per thread) and stored transposed into a 2-stage smem ring after the
+// k-tile's math (STS.32, lanes on consecutive rows: conflict-free); B streams
+// by cp.async as before.  8 x 16 outputs per thread, 128 threads.
+template <int CH, int ORDER>
+__global__ void __launch_bounds__(128, 2)
+sgemm_rowa(const float* __restrict__ A, const float* __restrict__ B, float* __restrict__ C, int M, int N, int K) {
+    constexpr int BM = 128, BN = 128, BK = 16, NT = 128, SB = 3;
+    extern __shared__ __align__(16) float sm[];
+    float* As = sm;                         // [2][BK][BM]
+    float* Bs = sm + 2 * BK * BM;           // [SB][BK][BN]
+    ulonglong2* Tot = reinterpret_cast<ulonglong2*>(Bs + SB * BK * BN);
+    const int t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31;
+    const int ty = warp * 4 + (lane >> 3);
+    const int tx = lane & 7;
+    const int tiles_n = N / BN, tiles_m = M / BM;
+    const int group = 16, bid = blockIdx.x, per_group = group * tiles_n;
+    const int g = bid / per_group, first_m = g * group;
+    const int gm = min(tiles_m - first_m, group);
+    const int tm = first_m + (bid % per_group) % gm, tn = (bid % per_group) / gm;
+    const int m0 = tm * BM, n0 = tn * BN;
+    // A: thread t owns row m0 + t (4 x 16 B of each k-tile)
+    const float4* Ag = reinterpret_cast<const float4*>(A + static_cast<long long>(m0 + t) * K);
+    const int c_row = t >> 5, c_col = (t & 31) * 4;
+    const float* Bg = B + static_cast<long long>(c_row) * N + n0 + c_col;
+    auto issue_b = [&](int kt, int stage) {
+        const long long kb = static_cast<long long>(kt) * BK * N;
+        float* bs = Bs + stage * BK * BN + c_row * BN + c_col;
+#pragma unroll
+        for (int r = 0; r < BK; r += 4) cp_async16(bs + r * BN, Bg + kb + static_cast<long long>(r) * N);
+    };
+    float4 ra[4];
+    auto load_a = [&](int kt) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) ra[c] = __ldg(Ag + kt * 4 + c);
+    };
+    auto store_a = [&](int stage) {
+        float* as = As + stage * BK * BM + t;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            as[(4 * c + 0) * BM] = ra[c].x;
+            as[(4 * c + 1) * BM] = ra[c].y;
+            as[(4 * c + 2) * BM] = ra[c].z;
+            as[(4 * c + 3) * BM] = ra[c].w;
+        }
+    };
+    unsigned long long acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0ull;
+    if constexpr (CH > 0) {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) Tot[q * NT + t] = make_ulonglong2(0ull, 0ull);
+    }
+    const int nk = K / BK;
+    load_a(0);
+    store_a(0);
+#pragma unroll
+    for (int s = 0; s < SB - 1; ++s) {
+        if (s < nk) issue_b(s, s);
+        cp_async_commit();
+    }
+    for (int kt = 0; kt < nk; ++kt) {
+        cp_async_wait<SB - 2>();
+        __syncthreads();
+        {
+            const int nt = kt + SB - 1;
+            if (nt < nk) issue_b(nt, nt % SB);
+            cp_async_commit();
+        }
+        if (kt + 1 < nk) load_a(kt + 1);
+        const float* as = As + (kt & 1) * BK * BM;
+        const float* bs = Bs + (kt % SB) * BK * BN;
+        float4 fa[2][2], fb[2][4];
+        fa[0][0] = *reinterpret_cast<const float4*>(as + ty * 4);
+        fa[0][1] = *reinterpret_cast<const float4*>(as + 64 + ty * 4);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) fb[0][c] = *reinterpret_cast<const float4*>(bs + c * 32 + tx * 4);
+#pragma unroll
+        for (int k = 0; k < BK; ++k) {
+            const int cur = k & 1, nxt = cur ^ 1;
+            if (k + 1 < BK) {
+                fa[nxt][0] = *reinterpret_cast<const float4*>(as + (k + 1) * BM + ty * 4);
+                fa[nxt][1] = *reinterpret_cast<const float4*>(as + (k + 1) * BM + 64 + ty * 4);
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    fb[nxt][c] = *reinterpret_cast<const float4*>(bs + (k + 1) * BN + c * 32 + tx * 4);
+            }
+            const float a[8] = {fa[cur][0].x, fa[cur][0].y, fa[cur][0].z, fa[cur][0].w,
+                                fa[cur][1].x, fa[cur][1].y, fa[cur][1].z, fa[cur][1].w};
+            unsigned long long b[8];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                b[2 * c] = pack2(fb[cur][c].x, fb[cur][c].y);
+                b[2 * c + 1] = pack2(fb[cur][c].z, fb[cur][c].w);
+            }
+            if (ORDER == 0) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const unsigned long long ai = pack2(a[i], a[i]);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) ffma2(acc[i][j], ai, b[j]);
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) ffma2(acc[i][j], pack2(a[i], a[i]), b[j]);
+            }
+        }
+        if (kt + 1 < nk) store_a((kt + 1) & 1);
+        if constexpr (CH > 0) {
+            if ((kt + 1) % CH == 0 || kt + 1 == nk) {
+                const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(Tot + t));
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        asm volatile(
+                            "{\n\t.reg .b64 t0, t1, t2, t3;\n\t"
+                            "ld.shared.v2.b64 {t0, t1}, [%4];\n\t"
+                            "ld.shared.v2.b64 {t2, t3}, [%4+2048];\n\t"
+                            "add.rn.f32x2 t0, t0, %0;\n\tadd.rn.f32x2 t1, t1, %1;\n\t"
+                            "add.rn.f32x2 t2, t2, %2;\n\tadd.rn.f32x2 t3, t3, %3;\n\t"
+                            "st.shared.v2.b64 [%4], {t0, t1};\n\t"
+                            "st.shared.v2.b64 [%4+2048], {t2, t3};\n\t"
+                            "mov.b64 %0, 0;\n\tmov.b64 %1, 0;\n\tmov.b64 %2, 0;\n\tmov.b64 %3, 0;\n\t}"
+                            : "+l"(acc[i][4 * h]), "+l"(acc[i][4 * h + 1]), "+l"(acc[i][4 * h + 2]),
+                              "+l"(acc[i][4 * h + 3])
+                            : "r"(base + static_cast<uint32_t>((4 * i + 2 * h) * NT * 16))
+                            : "memory");
+            }
+        }
+    }
+    cp_async_wait<0>();
+    if constexpr (CH > 0) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const ulonglong2 v = Tot[(4 * i + q) * NT + t];
+                acc[i][2 * q] = v.x;
+                acc[i][2 * q + 1] = v.y;
+            }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int row = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+        float* crow = C + static_cast<long long>(row) * N + n0 + tx * 4;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            *reinterpret_cast<ulonglong2*>(crow + c * 32) = make_ulonglong2(acc[i][2 * c], acc[i][2 * c + 1]);
+    }
+}
+
+__global__ void transpose(const float* __restrict__ A, float* __restrict__ At, int n) {
+    __shared__ float tile[32][33];
+    const int m0 = blockIdx.y * 32, k0 = blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int r = ty; r < 32; r += 8) tile[r][tx] = A[static_cast<long long>(m0 + r) * n + k0 + tx];
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) At[static_cast<long long>(k0 + r) * n + m0 + tx] = tile[tx][r];
+}
+
 template <typename Kern>
 static void run(const char* name, Kern k, int threads, int smem, const float* At, const float* B, float* C,
                 const float* Cref, int n, size_t bytes) {
@@ -314,20 +482,37 @@ __global__ void init(float* p, size_t n, uint32_t seed) {
 int main(int argc, char** argv) {
     int n = argc > 1 ? atoi(argv[1]) : 4096;
     size_t bytes = (size_t)n * n * 4;
-    float *At, *B, *C, *C0, *C1;
-    cudaMalloc(&At, bytes); cudaMalloc(&B, bytes); cudaMalloc(&C, bytes); cudaMalloc(&C0, bytes);
-    cudaMalloc(&C1, bytes);
-    init<<<1184, 256>>>(At, (size_t)n * n, 1);
+    float *A, *At, *B, *C, *C0, *C1, *C2;
+    cudaMalloc(&A, bytes); cudaMalloc(&At, bytes); cudaMalloc(&B, bytes); cudaMalloc(&C, bytes);
+    cudaMalloc(&C0, bytes); cudaMalloc(&C1, bytes); cudaMalloc(&C2, bytes);
+    init<<<1184, 256>>>(A, (size_t)n * n, 1);
     init<<<1184, 256>>>(B, (size_t)n * n, 2);
-    const int ring3 = 3 * 16 * 256 * 4, ring4 = 4 * 16 * 256 * 4;
+    transpose<<<dim3(n / 32, n / 32), 256>>>(A, At, n);
+    const int ring3 = 3 * 16 * 256 * 4;
+    const int rowa = (2 * 16 * 128 + 3 * 16 * 128) * 4;
+    const int tot = 32 * 128 * 16;
     run("product chain 8x8 k16s3", sgemm_v<16, 3>, 256, ring3, At, B, C0, nullptr, n, bytes);
-    run("8x16 chain k16s3 i-outer", sgemm_8x16<16, 3, 0, 0>, 128, ring3, At, B, C, C0, n, bytes);
-    run("8x16 chain k16s3 j-outer", sgemm_8x16<16, 3, 0, 1>, 128, ring3, At, B, C, C0, n, bytes);
-    run("8x16 chain k16s4 i-outer", sgemm_8x16<16, 4, 0, 0>, 128, ring4, At, B, C, C0, n, bytes);
-    run("8x16 chain k8s4 i-outer", sgemm_8x16<8, 4, 0, 0>, 128, 4 * 8 * 256 * 4, At, B, C, C0, n, bytes);
-    run("8x16 chain k32s2 i-outer", sgemm_8x16<32, 2, 0, 0>, 128, 2 * 32 * 256 * 4, At, B, C, C0, n, bytes);
-    run("8x16 blocked32 k16s3 i-outer", sgemm_8x16<16, 3, 32, 0>, 128, ring3 + 32 * 128 * 16, At, B, C1, nullptr,
-        n, bytes);
-    run("product chain 8x8 k16s3 (again)", sgemm_v<16, 3>, 256, ring3, At, B, C, C0, n, bytes);
+    run("8x16 chain j-outer", sgemm_8x16<16, 3, 0, 1>, 128, ring3, At, B, C, C0, n, bytes);
+    run("rowA 8x16 chain i-outer", sgemm_rowa<0, 0>, 128, rowa, A, B, C, C0, n, bytes);
+    run("rowA 8x16 chain j-outer", sgemm_rowa<0, 1>, 128, rowa, A, B, C, C0, n, bytes);
+    run("8x16 blocked32 j-outer", sgemm_8x16<16, 3, 32, 1>, 128, ring3 + tot, At, B, C1, nullptr, n, bytes);
+    run("8x16 blocked32 i-outer", sgemm_8x16<16, 3, 32, 0>, 128, ring3 + tot, At, B, C2, C1, n, bytes);
+    run("rowA 8x16 blocked32 i-outer", sgemm_rowa<32, 0>, 128, rowa + tot, A, B, C, C1, n, bytes);
+    run("rowA 8x16 blocked32 j-outer", sgemm_rowa<32, 1>, 128, rowa + tot, A, B, C, C1, n, bytes);
+    // the product kernel shape with blocked accumulation: 8x8, 256 threads (csrc/gemm_simt.cu)
+    {
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0); cudaEventCreate(&e1);
+        float best = 1e9;
+        for (int i = 0; i < 23; ++i) {
+            cudaEventRecord(e0);
+            transpose<<<dim3(n / 32, n / 32), 256>>>(A, At, n);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms; cudaEventElapsedTime(&ms, e0, e1);
+            if (i >= 3) best = ms < best ? ms : best;
+        }
+        printf("{\"variant\": \"A^T pre-pass alone\", \"ms_min\": %.4f}\n", best);
+    }
     return 0;
 }
