@@ -422,6 +422,153 @@ sgemm_rowa(const float* __restrict__ A, const float* __restrict__ B, float* __re
     }
 }
 
+// A read row-major through cp.async into an m-major smem tile ([128 m][16 k],
+// 16-byte chunks XOR-swizzled by (m >> 2) & 3): no A^T pre-pass.  A
+// fragments are LDS.128 over 4 consecutive k of each of the thread's 8 rows
+// (the same 2 LDS.128 per k-step as the k-major layout), loaded once per
+// group of 4 k-steps; B as before.  8 x 16 outputs per thread, j-outer.
+template <int CH>
+__global__ void __launch_bounds__(128, 2)
+sgemm_am(const float* __restrict__ A, const float* __restrict__ B, float* __restrict__ C, int M, int N, int K) {
+    constexpr int BM = 128, BN = 128, BK = 16, NT = 128, ST = 3;
+    extern __shared__ __align__(16) float sm[];
+    float* As = sm;                         // [ST][BM][BK] swizzled
+    float* Bs = sm + ST * BK * BM;          // [ST][BK][BN]
+    ulonglong2* Tot = reinterpret_cast<ulonglong2*>(Bs + ST * BK * BN);
+    const int t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31;
+    const int ty = warp * 4 + (lane >> 3);
+    const int tx = lane & 7;
+    const int sw = ty & 3;
+    const int tiles_n = N / BN, tiles_m = M / BM;
+    const int group = 16, bid = blockIdx.x, per_group = group * tiles_n;
+    const int g = bid / per_group, first_m = g * group;
+    const int gm = min(tiles_m - first_m, group);
+    const int tm = first_m + (bid % per_group) % gm, tn = (bid % per_group) / gm;
+    const int m0 = tm * BM, n0 = tn * BN;
+    // A copy: 4 consecutive threads move the 4 chunks of one row; rows (t >> 2) + 32 r
+    const int a_row = t >> 2, a_chk = t & 3;
+    const float* Ag = A + static_cast<long long>(m0 + a_row) * K + a_chk * 4;
+    const long long a32 = 32LL * K;
+    const int c_row = t >> 5, c_col = (t & 31) * 4;
+    const float* Bg = B + static_cast<long long>(c_row) * N + n0 + c_col;
+    auto issue = [&](int kt, int stage) {
+        float* as = As + stage * BK * BM;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int m = a_row + 32 * r;
+            cp_async16(as + m * BK + ((a_chk ^ ((m >> 2) & 3)) << 2), Ag + r * a32 + kt * BK);
+        }
+        const long long kb = static_cast<long long>(kt) * BK * N;
+        float* bs = Bs + stage * BK * BN + c_row * BN + c_col;
+#pragma unroll
+        for (int r = 0; r < BK; r += 4) cp_async16(bs + r * BN, Bg + kb + static_cast<long long>(r) * N);
+    };
+    unsigned long long acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0ull;
+    if constexpr (CH > 0) {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) Tot[q * NT + t] = make_ulonglong2(0ull, 0ull);
+    }
+    const int nk = K / BK;
+#pragma unroll
+    for (int s = 0; s < ST - 1; ++s) {
+        if (s < nk) issue(s, s);
+        cp_async_commit();
+    }
+    int arow[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) arow[i] = (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4)) * BK;
+    for (int kt = 0; kt < nk; ++kt) {
+        cp_async_wait<ST - 2>();
+        __syncthreads();
+        {
+            const int nt = kt + ST - 1;
+            if (nt < nk) issue(nt, nt % ST);
+            cp_async_commit();
+        }
+        const float* as = As + (kt % ST) * BK * BM;
+        const float* bs = Bs + (kt % ST) * BK * BN;
+        float4 fb[2][4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) fb[0][c] = *reinterpret_cast<const float4*>(bs + c * 32 + tx * 4);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            float4 a4[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a4[i] = *reinterpret_cast<const float4*>(as + arow[i] + ((q ^ sw) << 2));
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                const int k = 4 * q + kk;
+                const int cur = k & 1, nxt = cur ^ 1;
+                if (k + 1 < BK) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        fb[nxt][c] = *reinterpret_cast<const float4*>(bs + (k + 1) * BN + c * 32 + tx * 4);
+                }
+                float a[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    a[i] = kk == 0 ? a4[i].x : kk == 1 ? a4[i].y : kk == 2 ? a4[i].z : a4[i].w;
+                unsigned long long b[8];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    b[2 * c] = pack2(fb[cur][c].x, fb[cur][c].y);
+                    b[2 * c + 1] = pack2(fb[cur][c].z, fb[cur][c].w);
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) ffma2(acc[i][j], pack2(a[i], a[i]), b[j]);
+            }
+        }
+        if constexpr (CH > 0) {
+            if ((kt + 1) % CH == 0 || kt + 1 == nk) {
+                const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(Tot + t));
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        asm volatile(
+                            "{\n\t.reg .b64 t0, t1, t2, t3;\n\t"
+                            "ld.shared.v2.b64 {t0, t1}, [%4];\n\t"
+                            "ld.shared.v2.b64 {t2, t3}, [%4+2048];\n\t"
+                            "add.rn.f32x2 t0, t0, %0;\n\tadd.rn.f32x2 t1, t1, %1;\n\t"
+                            "add.rn.f32x2 t2, t2, %2;\n\tadd.rn.f32x2 t3, t3, %3;\n\t"
+                            "st.shared.v2.b64 [%4], {t0, t1};\n\t"
+                            "st.shared.v2.b64 [%4+2048], {t2, t3};\n\t"
+                            "mov.b64 %0, 0;\n\tmov.b64 %1, 0;\n\tmov.b64 %2, 0;\n\tmov.b64 %3, 0;\n\t}"
+                            : "+l"(acc[i][4 * h]), "+l"(acc[i][4 * h + 1]), "+l"(acc[i][4 * h + 2]),
+                              "+l"(acc[i][4 * h + 3])
+                            : "r"(base + static_cast<uint32_t>((4 * i + 2 * h) * NT * 16))
+                            : "memory");
+            }
+        }
+    }
+    cp_async_wait<0>();
+    if constexpr (CH > 0) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const ulonglong2 v = Tot[(4 * i + q) * NT + t];
+                acc[i][2 * q] = v.x;
+                acc[i][2 * q + 1] = v.y;
+            }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int row = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+        float* crow = C + static_cast<long long>(row) * N + n0 + tx * 4;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            *reinterpret_cast<ulonglong2*>(crow + c * 32) = make_ulonglong2(acc[i][2 * c], acc[i][2 * c + 1]);
+    }
+}
+
 __global__ void transpose(const float* __restrict__ A, float* __restrict__ At, int n) {
     __shared__ float tile[32][33];
     const int m0 = blockIdx.y * 32, k0 = blockIdx.x * 32;
@@ -489,16 +636,14 @@ int main(int argc, char** argv) {
     init<<<1184, 256>>>(B, (size_t)n * n, 2);
     transpose<<<dim3(n / 32, n / 32), 256>>>(A, At, n);
     const int ring3 = 3 * 16 * 256 * 4;
-    const int rowa = (2 * 16 * 128 + 3 * 16 * 128) * 4;
     const int tot = 32 * 128 * 16;
     run("product chain 8x8 k16s3", sgemm_v<16, 3>, 256, ring3, At, B, C0, nullptr, n, bytes);
     run("8x16 chain j-outer", sgemm_8x16<16, 3, 0, 1>, 128, ring3, At, B, C, C0, n, bytes);
-    run("rowA 8x16 chain i-outer", sgemm_rowa<0, 0>, 128, rowa, A, B, C, C0, n, bytes);
-    run("rowA 8x16 chain j-outer", sgemm_rowa<0, 1>, 128, rowa, A, B, C, C0, n, bytes);
+    run("A m-major 8x16 chain", sgemm_am<0>, 128, ring3, A, B, C, C0, n, bytes);
     run("8x16 blocked32 j-outer", sgemm_8x16<16, 3, 32, 1>, 128, ring3 + tot, At, B, C1, nullptr, n, bytes);
-    run("8x16 blocked32 i-outer", sgemm_8x16<16, 3, 32, 0>, 128, ring3 + tot, At, B, C2, C1, n, bytes);
-    run("rowA 8x16 blocked32 i-outer", sgemm_rowa<32, 0>, 128, rowa + tot, A, B, C, C1, n, bytes);
-    run("rowA 8x16 blocked32 j-outer", sgemm_rowa<32, 1>, 128, rowa + tot, A, B, C, C1, n, bytes);
+    run("A m-major 8x16 blocked32", sgemm_am<32>, 128, ring3 + tot, A, B, C, C1, n, bytes);
+    run("8x16 blocked32 j-outer (again)", sgemm_8x16<16, 3, 32, 1>, 128, ring3 + tot, At, B, C, C1, n, bytes);
+    run("A m-major 8x16 blocked32 (again)", sgemm_am<32>, 128, ring3 + tot, A, B, C, C1, n, bytes);
     // the product kernel shape with blocked accumulation: 8x8, 256 threads (csrc/gemm_simt.cu)
     {
         cudaEvent_t e0, e1;
