@@ -590,6 +590,10 @@ def run_hetft_arm(args, rank, world, local):
         except Exception as exc:  # noqa: BLE001
             return {"error": f"{type(exc).__name__}: {exc}"[:400]}
 
+    pcie = extra(pcie_step_bound, torch, nb, device)
+    if dmr is not None and pcie and "tasks_per_s" in pcie:
+        dmr["e2e"]["pcie_bound_frac"] = dmr["e2e"]["value"] / pcie["tasks_per_s"]
+
     c4x = None
     if not args.no_c3:
         if world >= 2 and not shared_gpu and torch.cuda.device_count() >= 2:
@@ -637,7 +641,10 @@ def run_hetft_arm(args, rank, world, local):
                 "note": "own window of max(80, steps) tasks with their own fault draws; the H2D of "
                         "step i+2 and the D2H of step i-1 overlap step i (PCIe: 192 MiB per step)",
                 "h2d_bytes_per_step": 2 * nb,
-                "d2h_bytes_per_step": nb},
+                "d2h_bytes_per_step": nb,
+                # the step's PCIe traffic alone, measured live: the e2e ceiling
+                "pcie_bound": dict(pcie, frac=((e2e_steps * world) / t_e2e) / (pcie["tasks_per_s"] * world))
+                if pcie and "tasks_per_s" in pcie else pcie},
         "gpu_launches": launches,
         "clocks": clocks,
         "roofline": {"bound": "fp32-simt", "kernel": "hf_gemm_simt (incl. A^T pre-pass), in-task",
@@ -663,6 +670,33 @@ def run_hetft_arm(args, rank, world, local):
         "peaks": {"source": peak_src, **peaks},
     }
     print(json.dumps(line), flush=True)
+
+
+def pcie_step_bound(torch, nb: int, device: int, iters: int = 5):
+    """The e2e step's host traffic alone on the copy engines: 2 x nb H2D on one
+    stream while nb D2H runs on another (pinned buffers), best of `iters`.
+    1 / that time bounds the e2e rate whatever the GPU does (tools/pcie_bw.py)."""
+    with torch.cuda.device(device):
+        hin = torch.empty(2 * nb, dtype=torch.uint8).pin_memory()
+        hout = torch.empty(nb, dtype=torch.uint8).pin_memory()
+        din = torch.empty(2 * nb, dtype=torch.uint8, device=f"cuda:{device}")
+        dout = torch.empty(nb, dtype=torch.uint8, device=f"cuda:{device}")
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        best = None
+        for _ in range(iters + 1):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            with torch.cuda.stream(s_in):
+                din[:nb].copy_(hin[:nb], non_blocking=True)
+                din[nb:].copy_(hin[nb:], non_blocking=True)
+            with torch.cuda.stream(s_out):
+                hout.copy_(dout, non_blocking=True)
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        del hin, hout, din, dout
+    return {"step_ms": best * 1e3, "tasks_per_s": 1.0 / best,
+            "shape": f"2 x {nb >> 20} MiB H2D + {nb >> 20} MiB D2H at once, pinned, copy engines"}
 
 
 def p2p_peak(src_dev: int, dst_dev: int, torch, nbytes: int = 1 << 30):
