@@ -58,7 +58,7 @@ def parse():
     ap.add_argument("--n", type=int, default=4096)
     ap.add_argument("--fault-prob", type=float, default=0.05, help="per-replica corrupt (bit flip) probability")
     ap.add_argument("--seed", type=int, default=1)
-    ap.add_argument("--e2e-steps", type=int, default=None, help="default max(80, --steps)")
+    ap.add_argument("--e2e-steps", type=int, default=None, help="default max(160, --steps)")
     ap.add_argument("--depth", type=int, default=1, help="TaskStream depth (tasks in flight beyond the one settling)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dmr", action="store_true", help="skip the HetDMR (configs[1]) side measurement")
@@ -545,7 +545,7 @@ def run_hetft_arm(args, rank, world, local):
     # ---- e2e: host buffers through the same API (H2D inside the stream, D2H read) ----
     # at least 80 steps: the pipeline fill (first 128 MiB H2D before any
     # kernel can start) and drain (last D2H) are paid once per timed region
-    e2e_steps = args.e2e_steps or max(80, args.steps)
+    e2e_steps = args.e2e_steps or max(160, args.steps)
     tmr.host_stream(2)
     torch.cuda.synchronize()
     barrier()
@@ -638,7 +638,7 @@ def run_hetft_arm(args, rank, world, local):
         "config": bench_config(args, world),
         "e2e": {"value": (e2e_steps * world) / t_e2e, "unit": "tasks/s", "steps": e2e_steps,
                 "rounds": e2e_rounds,
-                "note": "own window of max(80, steps) tasks with their own fault draws; the H2D of "
+                "note": "own window of max(160, steps) tasks with their own fault draws; the H2D of "
                         "step i+2 and the D2H of step i-1 overlap step i (PCIe: 192 MiB per step)",
                 "h2d_bytes_per_step": 2 * nb,
                 "d2h_bytes_per_step": nb,

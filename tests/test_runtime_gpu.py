@@ -379,10 +379,10 @@ def test_reserve_presizes_the_device_heap():
     rt = hf.Runtime(hf.load_fleet(cfg))
     nb = 48 << 20
     torch.cuda.synchronize()
-    reserved0 = torch.cuda.memory_stats().get("reserved_bytes.all.current", 0)
     rt.reserve("gpu0mem", nb, 6)
     stats = torch.cuda.memory_stats()
-    assert stats.get("reserved_bytes.all.current", 0) >= reserved0 + 6 * nb
+    # (the reserved total need not grow: earlier tests in the process may
+    # have left enough cached blocks; what matters is the next check)
     seg0 = stats.get("segment.all.allocated", 0)
     sp = rt.fleet.spaces["gpu0mem"]
     bufs = [rt.backend.alloc(sp, nb, zero=False) for _ in range(6)]
