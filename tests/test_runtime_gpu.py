@@ -563,3 +563,38 @@ def test_empty_areas_are_rejected_at_registration():
     with pytest.raises(hf.RegistrationError):
         rt.register_device_data(torch.empty(0, dtype=torch.uint8, device="cuda"), 0, hf.ValueType.FLOAT32, "r",
                                 "gpu0mem")
+
+
+def test_shared_gpu_lead_is_the_declared_costliest_variant_and_reads_wait_for_votes():
+    """Replicas sharing one GPU: the lead (LEAD_PRIORITY stream) is the variant
+    with the largest declared cost (the SIMT GEMM) on every round, whatever
+    the measured in-task timings say (r2b).  Votes run on the vote
+    stream; committed outputs read back right after each task of a pipelined
+    stream equal the SIMT kernel's own bytes (the reads wait on the vote)."""
+    from paper_1405_2912_b200.executor import LEAD_PRIORITY
+    rt, task = matmul_runtime(kinds=("gpu-tc", "gpu-simt", "gpu-tc3"), serial_replicas=True)
+    leads = []
+    orig = rt.backend.unit_stream
+
+    def spy(unit_id, device, priority=0, sync=True):
+        if priority == LEAD_PRIORITY:
+            leads.append(unit_id)
+        return orig(unit_id, device, priority=priority, sync=sync)
+    rt.backend.unit_stream = spy
+    n = 512
+    a, b = omatmul.make_inputs(n, seed=11)
+    ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    want = torch.empty(n, n, device="cuda")
+    kernels.gemm_simt(ta, tb, want)
+    want = want.cpu().numpy().tobytes()
+    outs = []
+    with rt.task_stream(depth=2) as ts:
+        for _ in range(8):
+            _, _, ic, args = register_mm(rt, a, b, device_inputs=True)
+            outs.append((ts.submit(task, args, hf.Strategy(hf.StrategyKind.HET_TMR)), ic))
+    assert len(leads) == 8 and set(leads) == {"gpu0.simt"}, leads
+    for rep, ic in outs:
+        assert rep.success and rep.votes == ["match"]
+        host = torch.empty(4 * n * n, dtype=torch.uint8).pin_memory()
+        rt.read_into(ic, host)
+        assert host.numpy().tobytes() == want
