@@ -569,6 +569,144 @@ sgemm_am(const float* __restrict__ A, const float* __restrict__ B, float* __rest
     }
 }
 
+// Early-barrier k-loop: the barrier that publishes tile kt+1 sits before the
+// last k-step of tile kt (whose fragments are already in registers), so the
+// first LDS.128s of tile kt+1 overlap that k-step's 64 FFMA2 instead of
+// following the barrier.  Stage kt is free after that barrier, so tile
+// kt+ST is issued into it: ST tiles in flight.  8x16 per thread, j-outer.
+template <int CH, int ST>
+__global__ void __launch_bounds__(128, 2)
+sgemm_early(const float* __restrict__ At, const float* __restrict__ B, float* __restrict__ C, int M, int N, int K) {
+    constexpr int BM = 128, BN = 128, BK = 16, NT = 128;
+    extern __shared__ __align__(16) float sm[];
+    float* As = sm;
+    float* Bs = sm + ST * BK * BM;
+    ulonglong2* Tot = reinterpret_cast<ulonglong2*>(Bs + ST * BK * BN);
+    const int t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31;
+    const int ty = warp * 4 + (lane >> 3);
+    const int tx = lane & 7;
+    const int tiles_n = N / BN, tiles_m = M / BM;
+    const int group = 16, bid = blockIdx.x, per_group = group * tiles_n;
+    const int g = bid / per_group, first_m = g * group;
+    const int gm = min(tiles_m - first_m, group);
+    const int tm = first_m + (bid % per_group) % gm, tn = (bid % per_group) / gm;
+    const int m0 = tm * BM, n0 = tn * BN;
+    const int c_row = t >> 5, c_col = (t & 31) * 4;
+    const float* Ag = At + static_cast<long long>(c_row) * M + m0 + c_col;
+    const float* Bg = B + static_cast<long long>(c_row) * N + n0 + c_col;
+    auto issue = [&](int kt, int stage) {
+        const long long ka = static_cast<long long>(kt) * BK * M;
+        const long long kb = static_cast<long long>(kt) * BK * N;
+        float* as = As + stage * BK * BM + c_row * BM + c_col;
+        float* bs = Bs + stage * BK * BN + c_row * BN + c_col;
+#pragma unroll
+        for (int r = 0; r < BK; r += 4) {
+            cp_async16(as + r * BM, Ag + ka + static_cast<long long>(r) * M);
+            cp_async16(bs + r * BN, Bg + kb + static_cast<long long>(r) * N);
+        }
+    };
+    unsigned long long acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0ull;
+    if constexpr (CH > 0) {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) Tot[q * NT + t] = make_ulonglong2(0ull, 0ull);
+    }
+    const int nk = K / BK;
+#pragma unroll
+    for (int s = 0; s < ST; ++s) {
+        if (s < nk) issue(s, s);
+        cp_async_commit();
+    }
+    cp_async_wait<ST - 1>();
+    __syncthreads();
+    float4 fa[2][2], fb[2][4];
+    auto load = [&](int buf, const float* as, const float* bs, int k) {
+        fa[buf][0] = *reinterpret_cast<const float4*>(as + k * BM + ty * 4);
+        fa[buf][1] = *reinterpret_cast<const float4*>(as + k * BM + 64 + ty * 4);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) fb[buf][c] = *reinterpret_cast<const float4*>(bs + k * BN + c * 32 + tx * 4);
+    };
+    auto compute = [&](int cur) {
+        const float a[8] = {fa[cur][0].x, fa[cur][0].y, fa[cur][0].z, fa[cur][0].w,
+                            fa[cur][1].x, fa[cur][1].y, fa[cur][1].z, fa[cur][1].w};
+        unsigned long long b[8];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            b[2 * c] = pack2(fb[cur][c].x, fb[cur][c].y);
+            b[2 * c + 1] = pack2(fb[cur][c].z, fb[cur][c].w);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) ffma2(acc[i][j], pack2(a[i], a[i]), b[j]);
+    };
+    load(0, As, Bs, 0);
+    for (int kt = 0; kt < nk; ++kt) {
+        const int st = kt % ST;
+        const float* as = As + st * BK * BM;
+        const float* bs = Bs + st * BK * BN;
+#pragma unroll
+        for (int k = 0; k < BK - 1; ++k) {
+            load((k + 1) & 1, as, bs, k + 1);
+            compute(k & 1);
+        }
+        if (kt + 1 < nk) {
+            cp_async_wait<ST - 2>();
+            __syncthreads();                          // tile kt+1 visible; stage st no longer read
+            if (kt + ST < nk) issue(kt + ST, st);
+            cp_async_commit();
+            const int nst = (kt + 1) % ST;
+            load(0, As + nst * BK * BM, Bs + nst * BK * BN, 0);
+        }
+        compute((BK - 1) & 1);
+        if constexpr (CH > 0) {
+            if ((kt + 1) % CH == 0 || kt + 1 == nk) {
+                const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(Tot + t));
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        asm volatile(
+                            "{\n\t.reg .b64 t0, t1, t2, t3;\n\t"
+                            "ld.shared.v2.b64 {t0, t1}, [%4];\n\t"
+                            "ld.shared.v2.b64 {t2, t3}, [%4+2048];\n\t"
+                            "add.rn.f32x2 t0, t0, %0;\n\tadd.rn.f32x2 t1, t1, %1;\n\t"
+                            "add.rn.f32x2 t2, t2, %2;\n\tadd.rn.f32x2 t3, t3, %3;\n\t"
+                            "st.shared.v2.b64 [%4], {t0, t1};\n\t"
+                            "st.shared.v2.b64 [%4+2048], {t2, t3};\n\t"
+                            "mov.b64 %0, 0;\n\tmov.b64 %1, 0;\n\tmov.b64 %2, 0;\n\tmov.b64 %3, 0;\n\t}"
+                            : "+l"(acc[i][4 * h]), "+l"(acc[i][4 * h + 1]), "+l"(acc[i][4 * h + 2]),
+                              "+l"(acc[i][4 * h + 3])
+                            : "r"(base + static_cast<uint32_t>((4 * i + 2 * h) * NT * 16))
+                            : "memory");
+            }
+        }
+    }
+    cp_async_wait<0>();
+    if constexpr (CH > 0) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const ulonglong2 v = Tot[(4 * i + q) * NT + t];
+                acc[i][2 * q] = v.x;
+                acc[i][2 * q + 1] = v.y;
+            }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int row = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+        float* crow = C + static_cast<long long>(row) * N + n0 + tx * 4;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            *reinterpret_cast<ulonglong2*>(crow + c * 32) = make_ulonglong2(acc[i][2 * c], acc[i][2 * c + 1]);
+    }
+}
+
 __global__ void transpose(const float* __restrict__ A, float* __restrict__ At, int n) {
     __shared__ float tile[32][33];
     const int m0 = blockIdx.y * 32, k0 = blockIdx.x * 32;
@@ -639,11 +777,13 @@ int main(int argc, char** argv) {
     const int tot = 32 * 128 * 16;
     run("product chain 8x8 k16s3", sgemm_v<16, 3>, 256, ring3, At, B, C0, nullptr, n, bytes);
     run("8x16 chain j-outer", sgemm_8x16<16, 3, 0, 1>, 128, ring3, At, B, C, C0, n, bytes);
-    run("A m-major 8x16 chain", sgemm_am<0>, 128, ring3, A, B, C, C0, n, bytes);
+    run("early chain s2", sgemm_early<0, 2>, 128, 2 * 16 * 256 * 4, At, B, C, C0, n, bytes);
+    run("early chain s3", sgemm_early<0, 3>, 128, ring3, At, B, C, C0, n, bytes);
     run("8x16 blocked32 j-outer", sgemm_8x16<16, 3, 32, 1>, 128, ring3 + tot, At, B, C1, nullptr, n, bytes);
-    run("A m-major 8x16 blocked32", sgemm_am<32>, 128, ring3 + tot, A, B, C, C1, n, bytes);
+    run("early blocked32 s2", sgemm_early<32, 2>, 128, 2 * 16 * 256 * 4 + tot, At, B, C, C1, n, bytes);
+    run("early blocked32 s3", sgemm_early<32, 3>, 128, ring3 + tot, At, B, C, C1, n, bytes);
     run("8x16 blocked32 j-outer (again)", sgemm_8x16<16, 3, 32, 1>, 128, ring3 + tot, At, B, C, C1, n, bytes);
-    run("A m-major 8x16 blocked32 (again)", sgemm_am<32>, 128, ring3 + tot, A, B, C, C1, n, bytes);
+    run("early blocked32 s3 (again)", sgemm_early<32, 3>, 128, ring3 + tot, At, B, C, C1, n, bytes);
     // the product kernel shape with blocked accumulation: 8x8, 256 threads (csrc/gemm_simt.cu)
     {
         cudaEvent_t e0, e1;
