@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--inputs", type=int, default=8, help="distinct (A, B) input pairs cycled over the tasks")
     ap.add_argument("--depth", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=8)
+    ap.add_argument("--gc", choices=("default", "freeze", "off"), default="default",
+                    help="Python cyclic GC during the timed region: as is, gc.freeze() after warm-up, or disabled")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--out", default=None)
     return ap.parse_args()
@@ -175,6 +177,13 @@ def main():
     if world > 1:
         dist.barrier()
     st = rt.backend.stream(dev)
+    import gc
+    if args.gc == "freeze":
+        gc.collect()
+        gc.freeze()
+    elif args.gc == "off":
+        gc.collect()
+        gc.disable()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     w0 = time.perf_counter()
     e0.record(st)
@@ -184,6 +193,7 @@ def main():
     e1.record(st)
     torch.cuda.synchronize()
     wall = time.perf_counter() - w0
+    gc.enable()
     t_dev = e0.elapsed_time(e1) * 1e-3
     keys = sorted(cnt)
     cd = "cpu" if shared_gpu else d
@@ -201,7 +211,7 @@ def main():
                 "seconds": t_job, "wall_s_rank0": wall, "scaling": "weak (tasks sharded t mod world)",
                 "config": {"workload": f"C5: {args.tasks} {args.strategy} tasks {n}x{n}, HBM checkpoint of "
                                        f"inputs, bit flips p={args.corrupt_prob}, aborts p={args.abort_prob} "
-                                       f"per replica attempt", "inputs": args.inputs, "depth": args.depth},
+                                       f"per replica attempt", "inputs": args.inputs, "depth": args.depth, "gc": args.gc},
                 "counts": tot,
                 "verify": "every committed C == binary64 A·B under the voter predicate (δ=1e-3), "
                           f"{tot['tasks'] - tot['verify_fail']}/{tot['tasks']} pass"}
