@@ -598,3 +598,50 @@ def test_shared_gpu_lead_is_the_declared_costliest_variant_and_reads_wait_for_vo
         host = torch.empty(4 * n * n, dtype=torch.uint8).pin_memory()
         rt.read_into(ic, host)
         assert host.numpy().tobytes() == want
+
+
+@pytest.mark.parametrize("depth", [None, 1])
+def test_nmr5_two_faulty_units_majority_commits_clean_simt_bytes(depth):
+    """K = 5 (Strategy(DMR, replicas=5): distinct units, variants may repeat)
+    on one GPU: two units flip one bit of every output they produce.  Every
+    element keeps a 3-of-5 majority, so the vote corrects; per-replica counts
+    are 1 for the two faulty slots and 0 elsewhere; the committed bytes equal
+    the clean SIMT kernel's output bit for bit (the vote lands in the lowest
+    fidelity-rank replica's buffer, and where that replica is faulty the
+    majority value comes from the clean SIMT replica)."""
+    cfg = hf.gpu_fleet_config(devices=(0,), kinds=("gpu-tc", "gpu-simt", "gpu-tc3"))
+    cfg["memory_spaces"].append({"id": "gpu0ckpt", "device": 0})
+    extra = [("gpu0.simt2", "gpu-simt"), ("gpu0.tc2", "gpu-tc")]
+    for uid, kind in extra:
+        cfg["units"].append({"id": uid, "kind": kind, "memory_space": "gpu0mem", "timing": "measured",
+                             "seed": 4242 + len(cfg["units"])})
+    faulty = {"gpu0.tc3": 27, "gpu0.simt2": 29}
+    for u in cfg["units"]:
+        if u["id"] in faulty:
+            u.update({"corrupt_prob": 1.0, "corrupt_mode": "bitflip", "corrupt_bit": faulty[u["id"]]})
+    rt = hf.Runtime(hf.load_fleet(cfg), hf.RuntimeConfig(checkpoint_space="gpu0ckpt", serial_replicas=True))
+    task = hf.get_workload("matmul").attach(rt)
+    n = 512
+    a, b = omatmul.make_inputs(n, seed=21)
+    ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    want = torch.empty(n, n, device="cuda")
+    kernels.gemm_simt(ta, tb, want)
+    want = want.cpu().numpy().tobytes()
+    strat = hf.Strategy(hf.StrategyKind.DMR, replicas=5)
+    reps = []
+    if depth is None:
+        for _ in range(3):
+            _, _, ic, args = register_mm(rt, a, b, device_inputs=True)
+            reps.append((rt.invoke(task, args, strat), ic))
+    else:
+        with rt.task_stream(depth=depth) as ts:
+            for _ in range(3):
+                _, _, ic, args = register_mm(rt, a, b, device_inputs=True)
+                reps.append((ts.submit(task, args, strat), ic))
+    for rep, ic in reps:
+        assert rep.success and rep.votes == ["corrected"], rep.votes
+        log = rep.rounds_log[-1]
+        assert len(log["slots"]) == 5
+        for slot, unit in enumerate(log["slots"]):
+            assert log["mismatch"][slot] == (1 if unit in faulty else 0), (unit, log["mismatch"])
+        assert rt.read_area(ic) == want
