@@ -775,6 +775,11 @@ int main(int argc, char** argv) {
     transpose<<<dim3(n / 32, n / 32), 256>>>(A, At, n);
     const int ring3 = 3 * 16 * 256 * 4;
     const int tot = 32 * 128 * 16;
+    if (argc > 2) {   // quick mode: the product's layout only (A/B of compiler flags)
+        run("8x16 blocked32 j-outer", sgemm_8x16<16, 3, 32, 1>, 128, ring3 + tot, At, B, C1, nullptr, n, bytes);
+        run("8x16 chain j-outer", sgemm_8x16<16, 3, 0, 1>, 128, ring3, At, B, C, nullptr, n, bytes);
+        return 0;
+    }
     run("product chain 8x8 k16s3", sgemm_v<16, 3>, 256, ring3, At, B, C0, nullptr, n, bytes);
     run("8x16 chain j-outer", sgemm_8x16<16, 3, 0, 1>, 128, ring3, At, B, C, C0, n, bytes);
     run("early chain s2", sgemm_early<0, 2>, 128, 2 * 16 * 256 * 4, At, B, C, C0, n, bytes);
