@@ -778,6 +778,11 @@ int main(int argc, char** argv) {
     if (argc > 2) {   // quick mode: the product's layout only (A/B of compiler flags)
         run("8x16 blocked32 j-outer", sgemm_8x16<16, 3, 32, 1>, 128, ring3 + tot, At, B, C1, nullptr, n, bytes);
         run("8x16 chain j-outer", sgemm_8x16<16, 3, 0, 1>, 128, ring3, At, B, C, nullptr, n, bytes);
+        run("8x16 blocked32 j-outer s2", sgemm_8x16<16, 2, 32, 1>, 128, 2 * 16 * 256 * 4 + tot, At, B, C, C1, n,
+            bytes);
+        run("8x16 blocked16 j-outer", sgemm_8x16<16, 3, 16, 1>, 128, ring3 + tot, At, B, C, nullptr, n, bytes);
+        run("8x16 blocked32 j-outer k8s4", sgemm_8x16<8, 4, 64, 1>, 128, 4 * 8 * 256 * 4 + tot, At, B, C, C1, n,
+            bytes);
         return 0;
     }
     run("product chain 8x8 k16s3", sgemm_v<16, 3>, 256, ring3, At, B, C0, nullptr, n, bytes);
