@@ -862,8 +862,9 @@ def _fp32_peak(sm_max_mhz: float):
                 raise ValueError(d.get("error"))
             return d["ffma2_tflops"], ("measured live: tools/fp32_peak (FFMA2 loop, 148x4 CTAs, best of 5; an 8x8 "
                                        "outer product issued b-pair-outer reaches it too, tools/ffma2_forms.cu); "
-                                       f"issued a-scalar-outer it peaks at {d['ffma2_bcast_tflops']:.1f}, which is "
-                                       "where ptxas's schedule of the GEMM lands")
+                                       f"issued a-scalar-outer it peaks at {d['ffma2_bcast_tflops']:.1f}; the "
+                                       "8x16 column-pair-outer GEMM loop reaches ~0.90 of the loop figure at "
+                                       "exact-wave shapes, tools/simt_fullwave.py)")
         except (OSError, ValueError, KeyError, IndexError, subprocess.SubprocessError):
             pass
     for p in sorted((ROOT / "profiles").glob("r*_fp32_peak.json"), reverse=True):
