@@ -265,6 +265,41 @@ def floats(n, start=0.0):
     return np.arange(start, start + n, dtype=np.float32).tobytes()
 
 
+class _WaitRecorder(HostBackend):
+    """Host double that records every (stream, event) wait."""
+
+    def __init__(self):
+        super().__init__()
+        self.waits = []
+
+    def wait(self, stream, event):
+        self.waits.append((stream, event))
+
+
+def test_readers_of_a_voted_area_wait_on_its_vote_once():
+    """Votes run on their own stream (CudaBackend.vote_stream), so the memory
+    manager orders the compute stream after a committed sibling's `ready`
+    event before the first copy-in, checkpoint or read of it, and only once
+    per commit (Sibling.ready_seen)."""
+    be = _WaitRecorder()
+    m = hf.MemoryManager(hf.load_fleet(three_units()), be)
+    a = m.register(floats(8), 8, hf.ValueType.FLOAT32, "w")
+    h = m.request(a, "gpu1mem", "w")
+    h.ready_event = "vote-event-1"
+    m.commit_success([h])
+    be.waits.clear()
+    m.request(a, "gpu1mem", "r")
+    m.request(a, "gpu1mem", "r", protect=True)      # sole copy: checkpointed, no second wait
+    m.request(a, "host", "r")
+    assert [e for _, e in be.waits] == ["vote-event-1"], be.waits
+    h2 = m.request(a, "gpu1mem", "w")
+    h2.ready_event = "vote-event-2"
+    m.commit_success([h2])
+    be.waits.clear()
+    m.request(a, "host", "r")
+    assert [e for _, e in be.waits] == ["vote-event-2"], be.waits
+
+
 class TestMemory:
     def test_sole_device_copy_backed_up_before_protected_write(self, mm):
         a = mm.register(floats(1000), 1000, hf.ValueType.FLOAT32, "w")
