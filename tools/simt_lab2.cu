@@ -707,6 +707,135 @@ sgemm_early(const float* __restrict__ At, const float* __restrict__ B, float* __
     }
 }
 
+// Rolling B fragments: one buffer of 4 float4 (16 registers instead of 32);
+// chunk c of step k+1 is loaded right after its last use in step k, 48
+// FFMA2 ahead of its next use.  A stays double-buffered.  8x16, j-outer,
+// blocked accumulation as the product.
+template <int CH>
+__global__ void __launch_bounds__(128, 2)
+sgemm_roll(const float* __restrict__ At, const float* __restrict__ B, float* __restrict__ C, int M, int N, int K) {
+    constexpr int BM = 128, BN = 128, BK = 16, NT = 128, ST = 3;
+    extern __shared__ __align__(16) float sm[];
+    float* As = sm;
+    float* Bs = sm + ST * BK * BM;
+    ulonglong2* Tot = reinterpret_cast<ulonglong2*>(Bs + ST * BK * BN);
+    const int t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31;
+    const int ty = warp * 4 + (lane >> 3);
+    const int tx = lane & 7;
+    const int tiles_n = N / BN, tiles_m = M / BM;
+    const int group = 16, bid = blockIdx.x, per_group = group * tiles_n;
+    const int g = bid / per_group, first_m = g * group;
+    const int gm = min(tiles_m - first_m, group);
+    const int tm = first_m + (bid % per_group) % gm, tn = (bid % per_group) / gm;
+    const int m0 = tm * BM, n0 = tn * BN;
+    const int c_row = t >> 5, c_col = (t & 31) * 4;
+    const float* Ag = At + static_cast<long long>(c_row) * M + m0 + c_col;
+    const float* Bg = B + static_cast<long long>(c_row) * N + n0 + c_col;
+    auto issue = [&](int kt, int stage) {
+        const long long ka = static_cast<long long>(kt) * BK * M;
+        const long long kb = static_cast<long long>(kt) * BK * N;
+        float* as = As + stage * BK * BM + c_row * BM + c_col;
+        float* bs = Bs + stage * BK * BN + c_row * BN + c_col;
+#pragma unroll
+        for (int r = 0; r < BK; r += 4) {
+            cp_async16(as + r * BM, Ag + ka + static_cast<long long>(r) * M);
+            cp_async16(bs + r * BN, Bg + kb + static_cast<long long>(r) * N);
+        }
+    };
+    unsigned long long acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0ull;
+    if constexpr (CH > 0) {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) Tot[q * NT + t] = make_ulonglong2(0ull, 0ull);
+    }
+    const int nk = K / BK;
+#pragma unroll
+    for (int s = 0; s < ST - 1; ++s) {
+        if (s < nk) issue(s, s);
+        cp_async_commit();
+    }
+    for (int kt = 0; kt < nk; ++kt) {
+        cp_async_wait<ST - 2>();
+        __syncthreads();
+        {
+            const int nt = kt + ST - 1;
+            if (nt < nk) issue(nt, nt % ST);
+            cp_async_commit();
+        }
+        const float* as = As + (kt % ST) * BK * BM;
+        const float* bs = Bs + (kt % ST) * BK * BN;
+        float4 fa[2][2], fb[4];
+        fa[0][0] = *reinterpret_cast<const float4*>(as + ty * 4);
+        fa[0][1] = *reinterpret_cast<const float4*>(as + 64 + ty * 4);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) fb[c] = *reinterpret_cast<const float4*>(bs + c * 32 + tx * 4);
+#pragma unroll
+        for (int k = 0; k < BK; ++k) {
+            const int cur = k & 1, nxt = cur ^ 1;
+            if (k + 1 < BK) {
+                fa[nxt][0] = *reinterpret_cast<const float4*>(as + (k + 1) * BM + ty * 4);
+                fa[nxt][1] = *reinterpret_cast<const float4*>(as + (k + 1) * BM + 64 + ty * 4);
+            }
+            const float a[8] = {fa[cur][0].x, fa[cur][0].y, fa[cur][0].z, fa[cur][0].w,
+                                fa[cur][1].x, fa[cur][1].y, fa[cur][1].z, fa[cur][1].w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const unsigned long long b0 = pack2(fb[c].x, fb[c].y), b1 = pack2(fb[c].z, fb[c].w);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) ffma2(acc[i][2 * c], pack2(a[i], a[i]), b0);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) ffma2(acc[i][2 * c + 1], pack2(a[i], a[i]), b1);
+                if (k + 1 < BK) fb[c] = *reinterpret_cast<const float4*>(bs + (k + 1) * BN + c * 32 + tx * 4);
+            }
+        }
+        if constexpr (CH > 0) {
+            if ((kt + 1) % CH == 0 || kt + 1 == nk) {
+                const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(Tot + t));
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        asm volatile(
+                            "{\n\t.reg .b64 t0, t1, t2, t3;\n\t"
+                            "ld.shared.v2.b64 {t0, t1}, [%4];\n\t"
+                            "ld.shared.v2.b64 {t2, t3}, [%4+2048];\n\t"
+                            "add.rn.f32x2 t0, t0, %0;\n\tadd.rn.f32x2 t1, t1, %1;\n\t"
+                            "add.rn.f32x2 t2, t2, %2;\n\tadd.rn.f32x2 t3, t3, %3;\n\t"
+                            "st.shared.v2.b64 [%4], {t0, t1};\n\t"
+                            "st.shared.v2.b64 [%4+2048], {t2, t3};\n\t"
+                            "mov.b64 %0, 0;\n\tmov.b64 %1, 0;\n\tmov.b64 %2, 0;\n\tmov.b64 %3, 0;\n\t}"
+                            : "+l"(acc[i][4 * h]), "+l"(acc[i][4 * h + 1]), "+l"(acc[i][4 * h + 2]),
+                              "+l"(acc[i][4 * h + 3])
+                            : "r"(base + static_cast<uint32_t>((4 * i + 2 * h) * NT * 16))
+                            : "memory");
+            }
+        }
+    }
+    cp_async_wait<0>();
+    if constexpr (CH > 0) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const ulonglong2 v = Tot[(4 * i + q) * NT + t];
+                acc[i][2 * q] = v.x;
+                acc[i][2 * q + 1] = v.y;
+            }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int row = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+        float* crow = C + static_cast<long long>(row) * N + n0 + tx * 4;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            *reinterpret_cast<ulonglong2*>(crow + c * 32) = make_ulonglong2(acc[i][2 * c], acc[i][2 * c + 1]);
+    }
+}
+
 __global__ void transpose(const float* __restrict__ A, float* __restrict__ At, int n) {
     __shared__ float tile[32][33];
     const int m0 = blockIdx.y * 32, k0 = blockIdx.x * 32;
@@ -778,6 +907,8 @@ int main(int argc, char** argv) {
     if (argc > 2) {   // quick mode: the product's layout only (A/B of compiler flags)
         run("8x16 blocked32 j-outer", sgemm_8x16<16, 3, 32, 1>, 128, ring3 + tot, At, B, C1, nullptr, n, bytes);
         run("8x16 chain j-outer", sgemm_8x16<16, 3, 0, 1>, 128, ring3, At, B, C, nullptr, n, bytes);
+        run("rolling-B blocked32", sgemm_roll<32>, 128, ring3 + tot, At, B, C, C1, n, bytes);
+        run("rolling-B chain", sgemm_roll<0>, 128, ring3, At, B, C, nullptr, n, bytes);
         run("8x16 blocked32 j-outer s2", sgemm_8x16<16, 2, 32, 1>, 128, 2 * 16 * 256 * 4 + tot, At, B, C, C1, n,
             bytes);
         run("8x16 blocked16 j-outer", sgemm_8x16<16, 3, 16, 1>, 128, ring3 + tot, At, B, C, nullptr, n, bytes);
